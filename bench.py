@@ -1,0 +1,301 @@
+"""LUT-KAN forward benchmark (BASELINE.json metric: edge-evals/s = batch x sum_l d_l*m_l).
+
+Default workload: BASELINE.json configs[1] ("C2"): KAN [78,16,2], G=5, L=64 int8 symmetric,
+closed + clip_x, 1,000,000 rows x 78 fp32 features per GPU (weak scaling: every rank runs
+its own 1M-row batch; the LUT is replicated). One step = one full chained forward of the
+batch. Inputs (312 MB/GPU) are larger than the 126 MB L2, so no flush is needed.
+
+`value` is device throughput with X resident in HBM; `e2e` is the same metric through the
+host-buffer entry point (lkg_model_forward_host: pinned X H2D, forward, Y D2H every step).
+`roofline` is the dominant kernel (layer-1 forward) against the shared-memory gather bound
+(see DESIGN.md §5). `cpu_baseline` times the reference CPU implementation (oracle/_ref =
+the reference's own sources, all host cores) on the same workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c2a|c3|c4] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+# workload -> (cfg, rows per GPU, L, scheme, boundary, policy)
+WORKLOADS = {
+    "c2": (2, 1_000_000, 64, 0, 1, 0),    # configs[1], int8 symmetric
+    "c2a": (2, 1_000_000, 64, 1, 1, 0),   # configs[1], uint8 asymmetric
+    "c3": (3, 262_144, 64, 0, 0, 0),      # configs[2] cell L=64 sym half_open clip_x
+    "c4": (4, 65_536, 64, 0, 0, 0),       # configs[3] (row count reduced per step)
+}
+SMEM_PEAK_GBS = 36600.0  # measured conflict-free LDS.128 throughput, tools/microbench (148 SMs)
+BYTES_PER_EE = {0: 6.0, 1: 10.0}  # algorithmic smem bytes per edge-eval
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.samples, self._stop = device, [], threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                self.samples.append([s.strip() for s in out.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples if len(s) >= 7 for i in range(4) if s[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def run_reference(args, wl):
+    """--impl reference: the reference CPU implementation of the path on the host cores."""
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return
+    from oracle.pyoracle import Oracle
+    cfg, rows, L, scheme, bm, op = WORKLOADS[wl]
+    o = Oracle("auto")
+    dims = o_dims(cfg)
+    chain = [o.compile_layer(o.recipe_layer(cfg, l), L, scheme, 1, 0, bm, op) for l in range(len(dims) - 1)]
+    ee_row = sum(dims[l] * dims[l + 1] for l in range(len(dims) - 1))
+    nthreads = os.cpu_count() or 1
+    sample_rows = sample_rows_for(ee_row, nthreads, rows)
+    X = o.recipe_inputs(cfg, 0, sample_rows).astype(np.float64)
+    for _ in range(args.warmup):
+        o.lut_model_forward(chain, X[: max(1, sample_rows // 10)], 1, nthreads)
+    t = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.lut_model_forward(chain, X, 1, nthreads)
+        t.append(time.perf_counter() - t0)
+    sec = sum(t) / len(t)
+    value = sample_rows * ee_row / sec
+    line = {"impl": "reference", "metric": "LUT-KAN forward edge-evals/s (batch x sum d*m)", "value": value,
+            "unit": "edge-evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (BASELINE recipe, reference Rng)",
+            "config": {"workload": wl, "cfg": f"configs[{cfg - 1}]", "dims": dims, "L": L,
+                       "scheme": ["int8_symmetric", "uint8_asymmetric"][scheme], "rows_per_step": sample_rows},
+            "cpu_baseline": {"value": value, "unit": "edge-evals/s", "cores": nthreads, "kind": o.kind,
+                             "sample": f"{sample_rows} rows of {wl} per step (reference lut_model_forward_batch, "
+                                       f"Tier::Optimized, rows sharded over {nthreads} threads)"},
+            "e2e": {"value": value, "unit": "edge-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def o_dims(cfg):
+    from oracle.pyoracle import RECIPE_DIMS
+    return RECIPE_DIMS[cfg]
+
+
+def sample_rows_for(ee_row, nthreads, rows, seconds=3.0):
+    """Rows the CPU reference processes in ~`seconds` (1.35e8 edge-evals/s per core)."""
+    return int(max(64, min(rows, seconds * 1.35e8 * max(1, nthreads * 0.6) / ee_row)))
+
+
+def cpu_baseline(wl):
+    from oracle.pyoracle import Oracle
+    cfg, rows, L, scheme, bm, op = WORKLOADS[wl]
+    o = Oracle("auto")
+    dims = o_dims(cfg)
+    chain = [o.compile_layer(o.recipe_layer(cfg, l), L, scheme, 1, 0, bm, op) for l in range(len(dims) - 1)]
+    ee_row = sum(dims[l] * dims[l + 1] for l in range(len(dims) - 1))
+    nthreads = os.cpu_count() or 1
+    n = sample_rows_for(ee_row, nthreads, rows, seconds=10.0)
+    X = o.recipe_inputs(cfg, 0, n).astype(np.float64)
+    o.lut_model_forward(chain, X[: max(1, n // 20)], 1, nthreads)
+    t0 = time.perf_counter()
+    o.lut_model_forward(chain, X, 1, nthreads)
+    sec = time.perf_counter() - t0
+    return {"value": n * ee_row / sec, "unit": "edge-evals/s", "cores": nthreads, "kind": o.kind,
+            "sample": f"{n} rows of {wl} (reference lut_model_forward_batch, Tier::Optimized, {nthreads} threads)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args, args.workload)
+        return
+
+    import torch
+    import paper_2601_03332_b200 as lk
+
+    rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    cfg, rows, L, scheme, bm, op = WORKLOADS[args.workload]
+    dims, G, _, _ = lk.recipe_dims(cfg)
+    nl = len(dims) - 1
+    ee_row = sum(dims[l] * dims[l + 1] for l in range(nl))
+    stream = torch.cuda.current_stream()
+    eng = lk.Engine(local, stream.cuda_stream)
+    qc = lk.QuantConfig(L, lk.Scheme(scheme), lk.Dtype(scheme))
+    oob = lk.OobConfig(lk.BoundaryMode(bm), lk.OobPolicy(op))
+    chain = [lk.compile_layer(lk.recipe_layer(cfg, l), qc, oob, engine=eng) for l in range(nl)]
+    dev = [a.device(eng) for a in chain]
+    import ctypes as C
+    from paper_2601_03332_b200._capi import OobStatsC, lib
+    handles = (C.c_void_p * nl)(*[d.handle for d in dev])
+
+    # this rank's batch: rows [rank*rows, (rank+1)*rows) of the recipe stream, pinned host + device copy
+    Xh = torch.empty((rows, dims[0]), dtype=torch.float32).pin_memory()
+    lk.recipe_inputs(cfg, rank * rows, rows, out=Xh.numpy())
+    Xd = Xh.to(f"cuda:{local}", non_blocking=False)
+    Yd = torch.empty((rows, dims[-1]), dtype=torch.float32, device=f"cuda:{local}")
+    Yh = torch.empty((rows, dims[-1]), dtype=torch.float32).pin_memory()
+
+    def step():
+        lk.lutkan.check(lib().lkg_model_forward(eng.handle, handles, nl, C.c_void_p(Xd.data_ptr()), rows,
+                                                C.c_void_p(Yd.data_ptr()), None))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    eng.collect(nl)
+    barrier()
+    launches0 = eng.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    launches = eng.launch_count - launches0
+    stats = eng.collect(nl)
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = world * rows * ee_row / (ms * 1e-3)
+
+    # dominant kernel: layer-1 forward, timed alone with events on the same stream
+    ms_l1 = None
+    big = max(range(nl), key=lambda l: dims[l] * dims[l + 1])
+    Hd = torch.empty((rows, dims[big + 1]), dtype=torch.float32, device=f"cuda:{local}")
+    Xin = Xd if big == 0 else torch.empty((rows, dims[big]), dtype=torch.float32, device=f"cuda:{local}").uniform_(-1, 1)
+    for _ in range(2):
+        lib().lkg_layer_forward(eng.handle, dev[big].handle, C.c_void_p(Xin.data_ptr()), rows, C.c_void_p(Hd.data_ptr()), None)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        lib().lkg_layer_forward(eng.handle, dev[big].handle, C.c_void_p(Xin.data_ptr()), rows, C.c_void_p(Hd.data_ptr()), None)
+    e1.record(stream)
+    barrier()
+    ms_l1 = e0.elapsed_time(e1) / args.steps
+    eng.collect(nl)
+    alg_bytes = rows * dims[big] * dims[big + 1] * BYTES_PER_EE[scheme]
+    achieved = alg_bytes / (ms_l1 * 1e-3) / 1e9
+    roofline = {"bound": "smem", "achieved": achieved, "peak": SMEM_PEAK_GBS, "unit": "GB/s",
+                "frac": achieved / SMEM_PEAK_GBS, "traffic": None,
+                "kernel": f"layer {big} forward ({dims[big]}->{dims[big + 1]}), {ms_l1:.4f} ms/launch",
+                "peak_source": "measured LDS.128 conflict-free throughput (tools/microbench/opbench.cu, 148 SMs); "
+                               "algorithmic bytes = 2 code B + 4 B scale (+4 B y_min asym) per edge-eval",
+                "edge_evals_per_s": rows * dims[big] * dims[big + 1] / (ms_l1 * 1e-3),
+                "share_of_step": ms_l1 / ms}
+
+    # end to end through the host-buffer entry point
+    e2e = None
+    if not args.no_e2e:
+        def host_step():
+            lk.lutkan.check(lib().lkg_model_forward_host(eng.handle, handles, nl, C.c_void_p(Xh.data_ptr()), rows,
+                                                         C.c_void_p(Yh.data_ptr()), None))
+        for _ in range(2):
+            host_step()
+        barrier()
+        k2 = max(3, min(args.steps, 10))
+        e0.record(stream)
+        for _ in range(k2):
+            host_step()
+        e1.record(stream)
+        barrier()
+        ms_e = e0.elapsed_time(e1) / k2
+        te = torch.tensor([ms_e], device=f"cuda:{local}")
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ms_e = float(te.item())
+        eng.collect(nl)
+        e2e = {"value": world * rows * ee_row / (ms_e * 1e-3), "unit": "edge-evals/s",
+               "h2d_bytes_per_step": rows * dims[0] * 4, "d2h_bytes_per_step": rows * dims[-1] * 4,
+               "ms_per_step": ms_e}
+
+    if rank == 0:
+        line = {"metric": "LUT-KAN forward edge-evals/s (batch x sum d*m)", "value": value, "unit": "edge-evals/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/i8 codes, fp32 math",
+                "data": "synthetic (BASELINE.json recipe, reference Rng; inputs > L2, no flush)",
+                "config": {"workload": args.workload, "cfg": f"configs[{cfg - 1}]", "dims": dims, "G": G, "L": L,
+                           "scheme": ["int8_symmetric", "uint8_asymmetric"][scheme],
+                           "boundary_mode": ["half_open", "closed"][bm], "oob_policy": ["clip_x", "zero_spline"][op],
+                           "rows_per_gpu": rows, "parallelism": f"batch dp{world}, LUT replicated",
+                           "l2": "inputs larger than L2 (no flush)"},
+                "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
+                "oob_any_frac_layer0": stats[0].oob_any_frac(), "clocks": clk.summary()}
+        if not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline(args.workload)
+            except Exception as ex:  # the oracle is optional on the box; say why it is missing
+                line["cpu_baseline"] = {"value": None, "error": repr(ex)}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

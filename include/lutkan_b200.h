@@ -1,0 +1,204 @@
+/*
+ * lutkan_b200.h — C-ABI of the B200-native LUT-KAN engine (liblutkan_b200.so).
+ *
+ * Drop-in boundary for the reference's hot path (namespace lutkan, /root/reference/proj/core):
+ *   compile    compile_layer / compile_model / compile_layer_debug_float  (compiler.hpp:67-77)
+ *   forward    lut_layer_forward_batch / lut_model_forward_batch          (runtime.hpp:130-148)
+ *   baseline   layer_forward_batch (spline, Tier::Optimized)              (spline.hpp:100-101)
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary. The
+ * C++ shim include/lutkan_b200.hpp re-exposes the reference signatures on top of it,
+ * and INTEGRATION.md shows the bindings a maintainer adds.
+ *
+ * Conventions
+ *  - Every function returns lkg_status; on failure lkg_last_error() (thread-local)
+ *    holds the message. Codes mirror the reference exception taxonomy
+ *    (types.hpp:11-39): CONFIG=ConfigError, DIMENSION=DimensionError,
+ *    NON_FINITE=NonFiniteError, UNSUPPORTED_BASE=UnsupportedBaseError.
+ *  - Enum values are the declaration order of types.hpp:41-49.
+ *  - Layouts are the reference's: edges input-major e = i*out_dim + j (spline.hpp:43),
+ *    q_table [E,K,L], scale/y_min [E,K], knots [K+1] (runtime.hpp:31-63).
+ *  - Device-resident objects (lkg_layer, lkg_spec) are immutable after creation and
+ *    may be shared by contexts on the same device. A context owns one CUDA stream;
+ *    all work is stream-ordered on it. Distinct contexts may be driven from distinct
+ *    host threads (the reference is pure and re-entrant).
+ *  - Documented differences from the reference: activations are fp32 on the device
+ *    (the reference's Matrix is f64; parity inputs are fp32-representable, so segment
+ *    indices and OOB masks are bit-exact); Tier is accepted by the C++ shim and
+ *    ignored (one backend, no CPU fallback).
+ */
+#ifndef LUTKAN_B200_H
+#define LUTKAN_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LKG_OK = 0,
+  LKG_ERR_CONFIG = 1,           /* lutkan::ConfigError */
+  LKG_ERR_DIMENSION = 2,        /* lutkan::DimensionError */
+  LKG_ERR_NON_FINITE = 3,       /* lutkan::NonFiniteError */
+  LKG_ERR_UNSUPPORTED_BASE = 4, /* lutkan::UnsupportedBaseError */
+  LKG_ERR_CUDA = 5,
+  LKG_ERR_NCCL = 6,
+  LKG_ERR_OOM = 7,
+  LKG_ERR_INVALID_ARG = 8
+} lkg_status;
+
+enum { LKG_SCHEME_SYMMETRIC = 0, LKG_SCHEME_ASYMMETRIC = 1 };      /* Scheme */
+enum { LKG_DTYPE_INT8 = 0, LKG_DTYPE_UINT8 = 1 };                  /* Dtype */
+enum { LKG_REPR_PHI = 0, LKG_REPR_SPLINE_COMPONENT = 1 };          /* ValueRepr */
+enum { LKG_INTERP_LINEAR = 0 };                                    /* Interp */
+enum { LKG_BOUNDARY_HALF_OPEN = 0, LKG_BOUNDARY_CLOSED = 1 };      /* BoundaryMode */
+enum { LKG_OOB_CLIP_X = 0, LKG_OOB_ZERO_SPLINE = 1 };              /* OobPolicy */
+enum { LKG_PARAM_F32 = 0, LKG_PARAM_F16 = 1 };                     /* ParamDtype */
+
+typedef struct lkg_ctx lkg_ctx;     /* device + stream + scratch (+ NCCL communicator) */
+typedef struct lkg_layer lkg_layer; /* device-resident LutLayerArtifact (or a column shard) */
+typedef struct lkg_spec lkg_spec;   /* device-resident KanLayerSpec (or a column shard) */
+
+/* OobStats, runtime.hpp:105-120. */
+typedef struct {
+  uint64_t n_samples, n_oob_samples, n_inputs, n_oob_inputs;
+} lkg_oob_stats;
+
+/* LutLayerArtifact fields (runtime.hpp:31-63), host pointers. Gains are required iff
+ * value_repr == spline_component; float_table (debug, [E,K,L] f64) is optional. */
+typedef struct {
+  int32_t in_dim, out_dim, K, L;
+  int32_t value_repr, interp, scheme, dtype, param_dtype, boundary_mode, oob_policy;
+  const char* base_kind; /* "silu" for spline_component, "" (or NULL) for phi */
+  const float* knots;
+  const uint8_t* q_table;
+  const float* scale;
+  const float* y_min;
+  const float* edge_base_scale;
+  const float* edge_spline_scale;
+  const float* edge_out_scale;
+  const double* float_table;
+} lkg_layer_desc;
+
+/* KanLayerSpec (spline.hpp:35-74), host pointers: f64 breakpoints [K+1], degree,
+ * packed_coeffs [E, K+degree], gains [E] (spline.hpp:57-62). */
+typedef struct {
+  int32_t in_dim, out_dim, K, degree;
+  const char* base_kind; /* only "silu" is registered (spline.cpp:105-108) */
+  const double* breakpoints;
+  const double* coeffs;
+  const double* base_scale;
+  const double* spline_scale;
+  const double* out_scale;
+} lkg_spec_desc;
+
+/* QuantConfig (compiler.hpp:15-24); OobConfig (runtime.hpp:19-22). */
+typedef struct {
+  int32_t L, scheme, dtype, value_repr, interp, param_dtype;
+} lkg_quant_config;
+typedef struct {
+  int32_t boundary_mode, oob_policy;
+} lkg_oob_config;
+
+/* Shape / footprint of a device layer (for reporting and download sizing). */
+typedef struct {
+  int32_t in_dim, out_dim, K, L, col0, col1, full_out_dim;
+  int32_t value_repr, scheme, param_dtype, boundary_mode, oob_policy, has_float_table;
+  uint64_t device_bytes;
+} lkg_layer_info;
+
+/* ------------------------------------------------------------------ context */
+const char* lkg_last_error(void);
+const char* lkg_version(void);
+/* stream: a cudaStream_t to run on (NULL = create a private non-blocking stream). */
+lkg_status lkg_ctx_create(int32_t device, void* stream, lkg_ctx** out);
+lkg_status lkg_ctx_destroy(lkg_ctx* ctx);
+lkg_status lkg_ctx_synchronize(lkg_ctx* ctx);
+void* lkg_ctx_stream(lkg_ctx* ctx);
+/* Number of kernels this context has launched so far (for bench's gpu_launches). */
+uint64_t lkg_ctx_launch_count(lkg_ctx* ctx);
+
+/* -------------------------------------------------------- artifact (F1, F2) */
+/* Validates like LutLayerArtifact::finalize (runtime.cpp:11-43) and uploads. */
+lkg_status lkg_layer_upload(lkg_ctx* ctx, const lkg_layer_desc* desc, lkg_layer** out);
+/* Column shard: only output columns [col0, col1) of desc (edges (i, j) with j in range),
+ * i.e. the strided slice {(i*m + j)*K*L ...} of the reference arrays. */
+lkg_status lkg_layer_upload_columns(lkg_ctx* ctx, const lkg_layer_desc* desc, int32_t col0,
+                                    int32_t col1, lkg_layer** out);
+lkg_status lkg_layer_info_get(const lkg_layer* layer, lkg_layer_info* out);
+/* Copies the layer back in the reference layout (sizes from lkg_layer_info: E = in_dim *
+ * (col1-col0)). Any output pointer may be NULL. */
+lkg_status lkg_layer_download(lkg_ctx* ctx, const lkg_layer* layer, float* knots, uint8_t* q_table,
+                              float* scale, float* y_min, float* edge_base_scale,
+                              float* edge_spline_scale, float* edge_out_scale, double* float_table);
+lkg_status lkg_layer_free(lkg_layer* layer);
+
+/* ------------------------------------------------------------ compile (CM*) */
+lkg_status lkg_spec_upload(lkg_ctx* ctx, const lkg_spec_desc* desc, lkg_spec** out);
+lkg_status lkg_spec_upload_columns(lkg_ctx* ctx, const lkg_spec_desc* desc, int32_t col0,
+                                   int32_t col1, lkg_spec** out);
+lkg_status lkg_spec_free(lkg_spec* spec);
+/* compile_layer (compiler.cpp:213-216): bytes, scales and y_mins bit-exact with the
+ * reference. keep_float != 0 also keeps the f64 float table (compile_layer_debug_float). */
+lkg_status lkg_compile_layer(lkg_ctx* ctx, const lkg_spec* spec, const lkg_quant_config* qc,
+                             const lkg_oob_config* oob, int32_t keep_float, lkg_layer** out);
+
+/* ----------------------------------------------------------- forward (F4-F15) */
+/* lut_layer_forward_batch (runtime.cpp:250-285): X [rows, in_dim] fp32 -> Y [rows, out_dim]
+ * fp32 (column shard: [rows, col1-col0]); both DEVICE pointers. If stats != NULL the call
+ * synchronizes, fills the layer's OobStats and reports NON_FINITE inputs; if stats == NULL
+ * it is asynchronous and counters accumulate until lkg_ctx_collect(). */
+lkg_status lkg_layer_forward(lkg_ctx* ctx, const lkg_layer* layer, const float* X, int64_t rows,
+                             float* Y, lkg_oob_stats* stats);
+/* lut_model_forward_batch (runtime.cpp:298-314): hidden activations stay on the device in
+ * fp32; stats (optional) is per layer [n_layers]. Chain checks as the reference. */
+lkg_status lkg_model_forward(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n_layers,
+                             const float* X, int64_t rows, float* Y, lkg_oob_stats* stats);
+/* Same call with HOST buffers (pinned or pageable): H2D of X, the chain, D2H of Y. */
+lkg_status lkg_model_forward_host(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n_layers,
+                                  const float* X_host, int64_t rows, float* Y_host,
+                                  lkg_oob_stats* stats);
+/* Per-element coordinates exactly as the forward kernels compute them (steps 1-4 of the
+ * 5-step pipeline, runtime.cpp:45-75 / 170-190): for x [n] fp32 (device), writes
+ * in-range mask, segment index k and sample index l0 (device int32 arrays, any may be NULL).
+ * Exposed so segment indices and OOB masks can be checked bit-exactly. */
+lkg_status lkg_layer_coords(lkg_ctx* ctx, const lkg_layer* layer, const float* x, int64_t n,
+                            int32_t* in_range, int32_t* k, int32_t* l0);
+/* Reads and resets the asynchronous OOB counters / non-finite flag of the last
+ * n_layers layer slots (slot l = l-th layer of the last chain). */
+lkg_status lkg_ctx_collect(lkg_ctx* ctx, lkg_oob_stats* stats, int32_t n_layers);
+
+/* ------------------------------------------------ spline baseline (S1, K3) */
+/* layer_forward_batch(spec, X, Tier::Optimized) (spline.cpp:145-187); device pointers. */
+lkg_status lkg_spline_forward(lkg_ctx* ctx, const lkg_spec* spec, const float* X, int64_t rows,
+                              float* Y);
+
+/* ------------------------------------------------ multi-GPU (column shards) */
+/* NCCL communicator for output-column sharding. id: 128 bytes from
+ * lkg_nccl_unique_id() on rank 0, broadcast by the host (e.g. torch.distributed). */
+lkg_status lkg_nccl_unique_id(uint8_t id_out[128]);
+lkg_status lkg_ctx_init_nccl(lkg_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank);
+/* Column-sharded chain: every rank holds the column shard [col0, col1) of every layer
+ * (equal shards, rank-ordered). X [rows, in_dim] replicated; between layers the local
+ * outputs are all-gathered over NCCL (rank-major blocks consumed in place); Y receives the
+ * last layer's LOCAL columns [rows, col1-col0]. */
+lkg_status lkg_model_forward_sharded(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n_layers,
+                                     const float* X, int64_t rows, float* Y, lkg_oob_stats* stats);
+
+/* ------------------------------------------------------- synthetic configs */
+/* The BASELINE.json configs (DESIGN.md §3 recipe; reference Rng, rng.hpp:13-58). cfg 1..5.
+ * dims_out receives n_layers+1 widths; returns n_layers in *n_layers. */
+lkg_status lkg_recipe_dims(int32_t cfg, int32_t* n_layers, int32_t* dims_out, int32_t* G,
+                           double* lo, double* hi);
+/* Host-side spec arrays of layer `layer` (caller-allocated: bp [G+1], coeffs [E*(G+3)],
+ * gains [E] x3). Restricted to columns [col0, col1) when col1 > col0. */
+lkg_status lkg_recipe_layer(int32_t cfg, int32_t layer, int32_t col0, int32_t col1,
+                            double* breakpoints, double* coeffs, double* base_scale,
+                            double* spline_scale, double* out_scale);
+/* fp32 inputs rows [row0, row0+rows). */
+lkg_status lkg_recipe_inputs(int32_t cfg, int64_t row0, int64_t rows, float* X);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

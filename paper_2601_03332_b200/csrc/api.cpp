@@ -1,0 +1,712 @@
+// api.cpp — host side of the C-ABI (include/lutkan_b200.h): validation mirroring the
+// reference (LutLayerArtifact::finalize runtime.cpp:11-43, QuantConfig::validate
+// compiler.cpp:10-16, KnotGrid/KanLayerSpec ctors spline.cpp:8-62, chain checks
+// runtime.cpp:298-304 / compiler.cpp:218-228), device residency, stream-ordered
+// launches, OOB-counter collection, host<->device entry points and the NCCL column-shard
+// chain. Errors map to lkg_status codes with a thread-local message.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "lkg_internal.h"
+
+namespace lkg {
+namespace {
+thread_local std::string g_err;
+}
+void set_error(const std::string& m) { g_err = m; }
+const char* last_error() { return g_err.c_str(); }
+}  // namespace lkg
+
+using lkg::DBuf;
+using lkg::Error;
+
+namespace {
+
+template <class F>
+lkg_status guarded(F&& f) {
+  try {
+    f();
+    return LKG_OK;
+  } catch (const Error& e) {
+    lkg::set_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    lkg::set_error("host allocation failed");
+    return LKG_ERR_OOM;
+  } catch (const std::exception& e) {
+    lkg::set_error(e.what());
+    return LKG_ERR_INVALID_ARG;
+  }
+}
+
+[[noreturn]] void fail(lkg_status c, const std::string& m) { throw Error{c, m}; }
+
+void need(const void* p, const char* what) {
+  if (!p) fail(LKG_ERR_INVALID_ARG, std::string("null pointer: ") + what);
+}
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) LKG_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+void check_knots(const float* knots, int K) {
+  if (K < 1) fail(LKG_ERR_CONFIG, "artifact needs at least 2 knots");
+  for (int i = 0; i <= K; i++) {
+    if (!std::isfinite(knots[i])) fail(LKG_ERR_NON_FINITE, "non-finite knot");
+    if (i > 0 && !(knots[i - 1] < knots[i])) fail(LKG_ERR_CONFIG, "knots must be strictly increasing");
+  }
+}
+
+void check_scheme(int scheme, int dtype) {
+  if (scheme == LKG_SCHEME_SYMMETRIC && dtype != LKG_DTYPE_INT8)
+    fail(LKG_ERR_CONFIG, "symmetric scheme requires int8");
+  if (scheme == LKG_SCHEME_ASYMMETRIC && dtype != LKG_DTYPE_UINT8)
+    fail(LKG_ERR_CONFIG, "asymmetric scheme requires uint8");
+  if (scheme != LKG_SCHEME_SYMMETRIC && scheme != LKG_SCHEME_ASYMMETRIC)
+    fail(LKG_ERR_CONFIG, "unknown scheme");
+}
+
+// LutLayerArtifact::finalize (runtime.cpp:11-43).
+void validate_desc(const lkg_layer_desc* d) {
+  need(d, "desc");
+  if (d->in_dim < 1 || d->out_dim < 1) fail(LKG_ERR_CONFIG, "artifact dims must be >= 1");
+  if (d->L < 2) fail(LKG_ERR_CONFIG, "samples per segment must be >= 2");
+  need(d->knots, "knots");
+  check_knots(d->knots, d->K);
+  check_scheme(d->scheme, d->dtype);
+  if (d->interp != LKG_INTERP_LINEAR) fail(LKG_ERR_CONFIG, "unknown interp");
+  if (d->boundary_mode != LKG_BOUNDARY_HALF_OPEN && d->boundary_mode != LKG_BOUNDARY_CLOSED)
+    fail(LKG_ERR_CONFIG, "unknown boundary_mode");
+  if (d->oob_policy != LKG_OOB_CLIP_X && d->oob_policy != LKG_OOB_ZERO_SPLINE)
+    fail(LKG_ERR_CONFIG, "unknown oob_policy");
+  if (d->param_dtype != LKG_PARAM_F32 && d->param_dtype != LKG_PARAM_F16)
+    fail(LKG_ERR_CONFIG, "unknown param_dtype");
+  need(d->q_table, "q_table");
+  need(d->scale, "scale");
+  need(d->y_min, "y_min");
+  if (d->value_repr == LKG_REPR_SPLINE_COMPONENT) {
+    if (!d->edge_base_scale || !d->edge_spline_scale || !d->edge_out_scale)
+      fail(LKG_ERR_DIMENSION, "edge scale arrays must have one entry per edge");
+    if (!d->base_kind || !*d->base_kind) fail(LKG_ERR_CONFIG, "spline_component artifact needs a base_kind");
+    if (std::strcmp(d->base_kind, "silu") != 0)
+      fail(LKG_ERR_UNSUPPORTED_BASE, std::string("unsupported base kind: \"") + d->base_kind + "\"");
+  } else if (d->value_repr == LKG_REPR_PHI) {
+    if (d->edge_base_scale || d->edge_spline_scale || d->edge_out_scale)
+      fail(LKG_ERR_CONFIG, "phi artifact must not carry edge scale arrays");
+  } else {
+    fail(LKG_ERR_CONFIG, "unknown value_repr");
+  }
+}
+
+// Strided column slice: for every input row i, columns [c0, c1) of a [d, m, inner] array.
+template <class T>
+void upload_cols(DBuf& dst, const T* src, int64_t d, int64_t m, int64_t inner, int c0, int c1,
+                 cudaStream_t st) {
+  const int64_t mc = c1 - c0;
+  dst.alloc(sizeof(T) * d * mc * inner);
+  if (!dst.bytes) return;
+  LKG_CUDA(cudaMemcpy2DAsync(dst.p, sizeof(T) * mc * inner, src + c0 * inner, sizeof(T) * m * inner,
+                             sizeof(T) * mc * inner, d, cudaMemcpyHostToDevice, st));
+}
+
+void ensure(DBuf& b, size_t bytes) {
+  if (b.bytes < bytes) b.alloc(bytes);
+}
+
+}  // namespace
+
+// ===================================================================== C-ABI
+extern "C" {
+
+const char* lkg_last_error(void) { return lkg::last_error(); }
+const char* lkg_version(void) { return "lutkan_b200 0.1 (sm_100a)"; }
+
+lkg_status lkg_ctx_create(int32_t device, void* stream, lkg_ctx** out) {
+  return guarded([&] {
+    need(out, "out");
+    int n = 0;
+    LKG_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) fail(LKG_ERR_INVALID_ARG, "no such CUDA device");
+    DeviceGuard g(device);
+    auto c = std::make_unique<lkg_ctx>();
+    c->device = device;
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      LKG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    c->counters.alloc(sizeof(uint64_t) * 4 * lkg_ctx::kSlots);
+    LKG_CUDA(cudaMemsetAsync(c->counters.p, 0, c->counters.bytes, c->stream));
+    LKG_CUDA(cudaStreamSynchronize(c->stream));
+    *out = c.release();
+  });
+}
+
+lkg_status lkg_ctx_destroy(lkg_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    DeviceGuard g(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl));
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+lkg_status lkg_ctx_synchronize(lkg_ctx* ctx) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+void* lkg_ctx_stream(lkg_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+uint64_t lkg_ctx_launch_count(lkg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ------------------------------------------------------------------- layers
+static lkg_status upload_impl(lkg_ctx* ctx, const lkg_layer_desc* d, int32_t col0, int32_t col1,
+                              lkg_layer** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    validate_desc(d);
+    if (col0 < 0 || col1 > d->out_dim || col1 <= col0) fail(LKG_ERR_DIMENSION, "bad column range");
+    DeviceGuard g(ctx->device);
+    auto L = std::make_unique<lkg_layer>();
+    L->device = ctx->device;
+    L->in_dim = d->in_dim;
+    L->out_dim = col1 - col0;
+    L->full_out_dim = d->out_dim;
+    L->col0 = col0;
+    L->col1 = col1;
+    L->K = d->K;
+    L->L = d->L;
+    L->value_repr = d->value_repr;
+    L->scheme = d->scheme;
+    L->param_dtype = d->param_dtype;
+    L->boundary_mode = d->boundary_mode;
+    L->oob_policy = d->oob_policy;
+    L->knots.assign(d->knots, d->knots + d->K + 1);
+    const int64_t din = d->in_dim, m = d->out_dim, K = d->K, Ls = d->L;
+    const int64_t E = din * (col1 - col0);
+    cudaStream_t st = ctx->stream;
+    upload_cols(L->q, d->q_table, din, m, K * Ls, col0, col1, st);
+    upload_cols(L->scale, d->scale, din, m, K, col0, col1, st);
+    upload_cols(L->ymin, d->y_min, din, m, K, col0, col1, st);
+    if (d->float_table) upload_cols(L->float_table, d->float_table, din, m, K * Ls, col0, col1, st);
+    if (d->value_repr == LKG_REPR_SPLINE_COMPONENT) {
+      L->gains.alloc(sizeof(float) * 3 * E);
+      const float* src[3] = {d->edge_base_scale, d->edge_spline_scale, d->edge_out_scale};
+      for (int t = 0; t < 3; t++)
+        LKG_CUDA(cudaMemcpy2DAsync(L->gains.as<float>() + t * E, sizeof(float) * (col1 - col0),
+                                   src[t] + col0, sizeof(float) * m, sizeof(float) * (col1 - col0), din,
+                                   cudaMemcpyHostToDevice, st));
+    }
+    lkg::launch_fuse_gains(ctx, L.get());
+    lkg::build_tiles(ctx, L.get());
+    LKG_CUDA(cudaStreamSynchronize(st));
+    *out = L.release();
+  });
+}
+
+lkg_status lkg_layer_upload(lkg_ctx* ctx, const lkg_layer_desc* desc, lkg_layer** out) {
+  return upload_impl(ctx, desc, 0, desc ? desc->out_dim : 0, out);
+}
+
+lkg_status lkg_layer_upload_columns(lkg_ctx* ctx, const lkg_layer_desc* desc, int32_t col0,
+                                    int32_t col1, lkg_layer** out) {
+  return upload_impl(ctx, desc, col0, col1, out);
+}
+
+lkg_status lkg_layer_info_get(const lkg_layer* L, lkg_layer_info* o) {
+  return guarded([&] {
+    need(L, "layer");
+    need(o, "out");
+    o->in_dim = L->in_dim;
+    o->out_dim = L->out_dim;
+    o->K = L->K;
+    o->L = L->L;
+    o->col0 = L->col0;
+    o->col1 = L->col1;
+    o->full_out_dim = L->full_out_dim;
+    o->value_repr = L->value_repr;
+    o->scheme = L->scheme;
+    o->param_dtype = L->param_dtype;
+    o->boundary_mode = L->boundary_mode;
+    o->oob_policy = L->oob_policy;
+    o->has_float_table = L->float_table.p != nullptr;
+    o->device_bytes = L->device_bytes();
+  });
+}
+
+lkg_status lkg_layer_download(lkg_ctx* ctx, const lkg_layer* L, float* knots, uint8_t* q, float* scale,
+                              float* y_min, float* bs, float* ss, float* os, double* ft) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(L, "layer");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const int64_t E = (int64_t)L->in_dim * L->out_dim;
+    if (knots) std::memcpy(knots, L->knots.data(), sizeof(float) * L->knots.size());
+    if (q) LKG_CUDA(cudaMemcpyAsync(q, L->q.p, L->q.bytes, cudaMemcpyDeviceToHost, st));
+    if (scale) LKG_CUDA(cudaMemcpyAsync(scale, L->scale.p, L->scale.bytes, cudaMemcpyDeviceToHost, st));
+    if (y_min) LKG_CUDA(cudaMemcpyAsync(y_min, L->ymin.p, L->ymin.bytes, cudaMemcpyDeviceToHost, st));
+    if (L->gains.p) {
+      float* dst[3] = {bs, ss, os};
+      for (int t = 0; t < 3; t++)
+        if (dst[t])
+          LKG_CUDA(cudaMemcpyAsync(dst[t], L->gains.as<float>() + t * E, sizeof(float) * E,
+                                   cudaMemcpyDeviceToHost, st));
+    }
+    if (ft && L->float_table.p)
+      LKG_CUDA(cudaMemcpyAsync(ft, L->float_table.p, L->float_table.bytes, cudaMemcpyDeviceToHost, st));
+    LKG_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
+lkg_status lkg_layer_free(lkg_layer* L) {
+  return guarded([&] {
+    if (!L) return;
+    DeviceGuard g(L->device);
+    delete L;
+  });
+}
+
+// -------------------------------------------------------------------- specs
+static lkg_status spec_upload_impl(lkg_ctx* ctx, const lkg_spec_desc* d, int32_t col0, int32_t col1,
+                                   lkg_spec** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    need(d, "desc");
+    // KnotGrid (spline.cpp:8-27) and KanLayerSpec (spline.cpp:29-62) validation.
+    if (d->degree < 0) fail(LKG_ERR_CONFIG, "degree must be >= 0");
+    if (d->K < 1) fail(LKG_ERR_CONFIG, "need at least 2 breakpoints");
+    need(d->breakpoints, "breakpoints");
+    for (int i = 0; i <= d->K; i++) {
+      if (!std::isfinite(d->breakpoints[i])) fail(LKG_ERR_NON_FINITE, "non-finite breakpoint");
+      if (i > 0 && !(d->breakpoints[i - 1] < d->breakpoints[i]))
+        fail(LKG_ERR_CONFIG, "breakpoints must be strictly increasing");
+    }
+    if (d->in_dim < 1 || d->out_dim < 1) fail(LKG_ERR_CONFIG, "layer dims must be >= 1");
+    if (col0 < 0 || col1 > d->out_dim || col1 <= col0) fail(LKG_ERR_DIMENSION, "bad column range");
+    need(d->coeffs, "coeffs");
+    need(d->base_scale, "base_scale");
+    need(d->spline_scale, "spline_scale");
+    need(d->out_scale, "out_scale");
+    if (d->base_kind && std::strcmp(d->base_kind, "silu") != 0)
+      fail(LKG_ERR_UNSUPPORTED_BASE, std::string("unsupported base kind: \"") + d->base_kind + "\"");
+    const int64_t din = d->in_dim, m = d->out_dim, R = d->K + d->degree, mc = col1 - col0;
+    for (int64_t i = 0; i < din; i++)
+      for (int64_t j = col0; j < col1; j++) {
+        const int64_t e = i * m + j;
+        for (int64_t r = 0; r < R; r++)
+          if (!std::isfinite(d->coeffs[e * R + r])) fail(LKG_ERR_NON_FINITE, "non-finite spline coefficient");
+        if (!std::isfinite(d->base_scale[e]) || !std::isfinite(d->spline_scale[e]) ||
+            !std::isfinite(d->out_scale[e]))
+          fail(LKG_ERR_NON_FINITE, "non-finite edge scale");
+      }
+    DeviceGuard g(ctx->device);
+    auto S = std::make_unique<lkg_spec>();
+    S->device = ctx->device;
+    S->in_dim = d->in_dim;
+    S->out_dim = (int32_t)mc;
+    S->full_out_dim = d->out_dim;
+    S->col0 = col0;
+    S->col1 = col1;
+    S->K = d->K;
+    S->degree = d->degree;
+    S->breakpoints.assign(d->breakpoints, d->breakpoints + d->K + 1);
+    cudaStream_t st = ctx->stream;
+    upload_cols(S->coeffs, d->coeffs, din, m, R, col0, col1, st);
+    const int64_t E = din * mc;
+    S->gains.alloc(sizeof(double) * 3 * E);
+    const double* src[3] = {d->base_scale, d->spline_scale, d->out_scale};
+    for (int t = 0; t < 3; t++)
+      LKG_CUDA(cudaMemcpy2DAsync(S->gains.as<double>() + t * E, sizeof(double) * mc, src[t] + col0,
+                                 sizeof(double) * m, sizeof(double) * mc, din, cudaMemcpyHostToDevice, st));
+    S->col0 = 0;  // device arrays hold only the shard; keep the original range for info
+    S->col1 = (int32_t)mc;
+    lkg::launch_spec_prepare(ctx, S.get());
+    LKG_CUDA(cudaStreamSynchronize(st));
+    *out = S.release();
+  });
+}
+
+lkg_status lkg_spec_upload(lkg_ctx* ctx, const lkg_spec_desc* desc, lkg_spec** out) {
+  return spec_upload_impl(ctx, desc, 0, desc ? desc->out_dim : 0, out);
+}
+lkg_status lkg_spec_upload_columns(lkg_ctx* ctx, const lkg_spec_desc* desc, int32_t col0, int32_t col1,
+                                   lkg_spec** out) {
+  return spec_upload_impl(ctx, desc, col0, col1, out);
+}
+lkg_status lkg_spec_free(lkg_spec* S) {
+  return guarded([&] {
+    if (!S) return;
+    DeviceGuard g(S->device);
+    delete S;
+  });
+}
+
+// ------------------------------------------------------------------ compile
+lkg_status lkg_compile_layer(lkg_ctx* ctx, const lkg_spec* S, const lkg_quant_config* qc,
+                             const lkg_oob_config* oob, int32_t keep_float, lkg_layer** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(S, "spec");
+    need(qc, "quant config");
+    need(oob, "oob config");
+    need(out, "out");
+    // QuantConfig::validate (compiler.cpp:10-16)
+    if (qc->L < 2) fail(LKG_ERR_CONFIG, "samples_per_segment must be >= 2");
+    check_scheme(qc->scheme, qc->dtype);
+    if (qc->value_repr != LKG_REPR_PHI && qc->value_repr != LKG_REPR_SPLINE_COMPONENT)
+      fail(LKG_ERR_CONFIG, "unknown value_repr");
+    if (qc->param_dtype != LKG_PARAM_F32 && qc->param_dtype != LKG_PARAM_F16)
+      fail(LKG_ERR_CONFIG, "unknown param_dtype");
+    if (oob->boundary_mode != LKG_BOUNDARY_HALF_OPEN && oob->boundary_mode != LKG_BOUNDARY_CLOSED)
+      fail(LKG_ERR_CONFIG, "unknown boundary_mode");
+    if (oob->oob_policy != LKG_OOB_CLIP_X && oob->oob_policy != LKG_OOB_ZERO_SPLINE)
+      fail(LKG_ERR_CONFIG, "unknown oob_policy");
+    DeviceGuard g(ctx->device);
+    const int K = S->K, Ls = qc->L, p = S->degree, R = K + p;
+    // Sample points and exact f64 basis windows (build_float_lut, compiler.cpp:29-57).
+    std::vector<double> ext;
+    lkg::knot_grid(S->breakpoints, p, ext);
+    const int64_t npts = (int64_t)K * Ls;
+    std::vector<double> full((size_t)npts * R), buf(R + p + 1), silu((size_t)npts, 0.0);
+    std::vector<int32_t> first((size_t)npts), last((size_t)npts);
+    for (int k = 0; k < K; k++) {
+      const double t0 = S->breakpoints[k];
+      const double step = (S->breakpoints[k + 1] - t0) / static_cast<double>(Ls);
+      for (int l = 0; l < Ls; l++) {
+        const int64_t pi = (int64_t)k * Ls + l;
+        const double x = t0 + static_cast<double>(l) * step;
+        lkg::basis_into(ext, p, x, buf.data());
+        std::copy(buf.begin(), buf.begin() + R, full.begin() + pi * R);
+        int f = R, la = -1;
+        for (int r = 0; r < R; r++)
+          if (buf[r] != 0.0) {
+            f = std::min(f, r);
+            la = r;
+          }
+        first[pi] = f == R ? 0 : f;
+        last[pi] = la < 0 ? 0 : la;
+        if (qc->value_repr == LKG_REPR_PHI) silu[pi] = lkg::silu_host(x);
+      }
+    }
+    int W = 1;
+    for (int64_t pi = 0; pi < npts; pi++) W = std::max(W, last[pi] - first[pi] + 1);
+    std::vector<int32_t> r0((size_t)npts);
+    std::vector<double> win((size_t)npts * W, 0.0);
+    for (int64_t pi = 0; pi < npts; pi++) {
+      int s = std::min(first[pi], R - W);
+      r0[pi] = s;
+      for (int t = 0; t < W; t++) win[pi * W + t] = full[pi * R + s + t];
+    }
+    DBuf d_basis, d_r0, d_silu;
+    d_basis.alloc(sizeof(double) * win.size());
+    d_r0.alloc(sizeof(int32_t) * r0.size());
+    d_silu.alloc(sizeof(double) * silu.size());
+    cudaStream_t st = ctx->stream;
+    LKG_CUDA(cudaMemcpyAsync(d_basis.p, win.data(), d_basis.bytes, cudaMemcpyHostToDevice, st));
+    LKG_CUDA(cudaMemcpyAsync(d_r0.p, r0.data(), d_r0.bytes, cudaMemcpyHostToDevice, st));
+    LKG_CUDA(cudaMemcpyAsync(d_silu.p, silu.data(), d_silu.bytes, cudaMemcpyHostToDevice, st));
+
+    auto L = std::make_unique<lkg_layer>();
+    L->device = ctx->device;
+    L->in_dim = S->in_dim;
+    L->out_dim = S->col1 - S->col0;
+    L->full_out_dim = S->full_out_dim;
+    L->col0 = 0;
+    L->col1 = L->out_dim;
+    L->K = K;
+    L->L = Ls;
+    L->value_repr = qc->value_repr;
+    L->scheme = qc->scheme;
+    L->param_dtype = qc->param_dtype;
+    L->boundary_mode = oob->boundary_mode;
+    L->oob_policy = oob->oob_policy;
+    L->knots.resize(K + 1);
+    for (int i = 0; i <= K; i++) L->knots[i] = static_cast<float>(S->breakpoints[i]);
+    check_knots(L->knots.data(), K);  // finalize(): f32 knots must stay strictly increasing
+    const int64_t E = (int64_t)L->in_dim * L->out_dim;
+    L->q.alloc((size_t)E * K * Ls);
+    L->scale.alloc(sizeof(float) * E * K);
+    L->ymin.alloc(sizeof(float) * E * K);
+    if (keep_float) L->float_table.alloc(sizeof(double) * E * K * Ls);
+    if (qc->value_repr == LKG_REPR_SPLINE_COMPONENT) L->gains.alloc(sizeof(float) * 3 * E);
+    lkg::launch_compile(ctx, S, qc, L.get(), d_basis.as<double>(), d_r0.as<int32_t>(),
+                        d_silu.as<double>(), W, keep_float != 0);
+    lkg::launch_fuse_gains(ctx, L.get());
+    lkg::build_tiles(ctx, L.get());
+    LKG_CUDA(cudaStreamSynchronize(st));
+    *out = L.release();
+  });
+}
+
+// ------------------------------------------------------------------ forward
+static void reset_slots(lkg_ctx* ctx, int n) {
+  LKG_CUDA(cudaMemsetAsync(ctx->counters.p, 0, sizeof(uint64_t) * 4 * n, ctx->stream));
+  for (int s = 0; s < n; s++) {
+    ctx->rows_seen[s] = 0;
+    ctx->in_dim_seen[s] = 0;
+  }
+}
+
+static void collect_impl(lkg_ctx* ctx, lkg_oob_stats* stats, int n) {
+  if (n > lkg_ctx::kSlots) fail(LKG_ERR_INVALID_ARG, "too many layer slots");
+  std::vector<uint64_t> h(4 * (size_t)n);
+  LKG_CUDA(cudaMemcpyAsync(h.data(), ctx->counters.p, sizeof(uint64_t) * h.size(), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  bool nonfinite = false;
+  for (int s = 0; s < n; s++) {
+    nonfinite |= h[4 * s + 2] != 0;
+    if (stats) {
+      stats[s].n_samples = ctx->rows_seen[s];
+      stats[s].n_oob_samples = h[4 * s + 0];
+      stats[s].n_inputs = ctx->rows_seen[s] * (uint64_t)ctx->in_dim_seen[s];
+      stats[s].n_oob_inputs = h[4 * s + 1];
+    }
+  }
+  reset_slots(ctx, n);
+  if (nonfinite) fail(LKG_ERR_NON_FINITE, "non-finite input value");
+}
+
+static void check_chain(const lkg_layer* const* chain, int n) {
+  if (n < 1 || !chain) fail(LKG_ERR_CONFIG, "artifact chain is empty");
+  if (n > lkg_ctx::kSlots) fail(LKG_ERR_CONFIG, "artifact chain too long");
+  for (int l = 0; l < n; l++)
+    if (!chain[l]) fail(LKG_ERR_INVALID_ARG, "null layer in chain");
+}
+
+static void run_chain(lkg_ctx* ctx, const lkg_layer* const* chain, int n, const float* X, int64_t rows,
+                      float* Y) {
+  for (int l = 1; l < n; l++)
+    if (chain[l]->in_dim != chain[l - 1]->out_dim)
+      fail(LKG_ERR_DIMENSION, "artifact chain dimension mismatch between layers " + std::to_string(l - 1) +
+                                  " and " + std::to_string(l));
+  size_t hid = 0;
+  for (int l = 0; l + 1 < n; l++) hid = std::max(hid, (size_t)chain[l]->out_dim);
+  if (n > 1) {
+    ensure(ctx->scratch[0], sizeof(float) * rows * hid);
+    ensure(ctx->scratch[1], sizeof(float) * rows * hid);
+  }
+  const float* cur = X;
+  for (int l = 0; l < n; l++) {
+    float* dst = l == n - 1 ? Y : ctx->scratch[l & 1].as<float>();
+    lkg::launch_forward(ctx, chain[l], cur, rows, 0, dst, l, true);
+    ctx->rows_seen[l] += (uint64_t)rows;
+    ctx->in_dim_seen[l] = chain[l]->in_dim;
+    cur = dst;
+  }
+}
+
+lkg_status lkg_layer_forward(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, float* Y,
+                             lkg_oob_stats* stats) {
+  const lkg_layer* chain[1] = {L};
+  return lkg_model_forward(ctx, chain, 1, X, rows, Y, stats);
+}
+
+lkg_status lkg_model_forward(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n, const float* X,
+                             int64_t rows, float* Y, lkg_oob_stats* stats) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    check_chain(chain, n);
+    if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
+    if (rows > 0) {
+      need(X, "X");
+      need(Y, "Y");
+    }
+    DeviceGuard g(ctx->device);
+    run_chain(ctx, chain, n, X, rows, Y);
+    if (stats) collect_impl(ctx, stats, n);
+  });
+}
+
+lkg_status lkg_model_forward_host(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n, const float* Xh,
+                                  int64_t rows, float* Yh, lkg_oob_stats* stats) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    check_chain(chain, n);
+    if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
+    DeviceGuard g(ctx->device);
+    const size_t xb = sizeof(float) * rows * chain[0]->in_dim, yb = sizeof(float) * rows * chain[n - 1]->out_dim;
+    ensure(ctx->hostio, xb + yb + 256);
+    float* dX = ctx->hostio.as<float>();
+    float* dY = reinterpret_cast<float*>(ctx->hostio.as<char>() + ((xb + 255) / 256) * 256);
+    if (rows > 0) {
+      need(Xh, "X");
+      need(Yh, "Y");
+      LKG_CUDA(cudaMemcpyAsync(dX, Xh, xb, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    run_chain(ctx, chain, n, dX, rows, dY);
+    if (rows > 0) LKG_CUDA(cudaMemcpyAsync(Yh, dY, yb, cudaMemcpyDeviceToHost, ctx->stream));
+    if (stats) collect_impl(ctx, stats, n);
+    else LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+lkg_status lkg_layer_coords(lkg_ctx* ctx, const lkg_layer* L, const float* x, int64_t n, int32_t* in_range,
+                            int32_t* k, int32_t* l0) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(L, "layer");
+    if (n < 0) fail(LKG_ERR_DIMENSION, "negative count");
+    if (n > 0) need(x, "x");
+    DeviceGuard g(ctx->device);
+    lkg::launch_coords(ctx, L, x, n, in_range, k, l0);
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+lkg_status lkg_ctx_collect(lkg_ctx* ctx, lkg_oob_stats* stats, int32_t n) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    DeviceGuard g(ctx->device);
+    collect_impl(ctx, stats, n);
+  });
+}
+
+lkg_status lkg_spline_forward(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows, float* Y) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(S, "spec");
+    if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
+    if (rows == 0) return;
+    need(X, "X");
+    need(Y, "Y");
+    DeviceGuard g(ctx->device);
+    lkg::launch_spline(ctx, S, X, rows, Y, nullptr);
+  });
+}
+
+// ---------------------------------------------------------------- multi-GPU
+lkg_status lkg_nccl_unique_id(uint8_t id_out[128]) {
+  return guarded([&] {
+    need(id_out, "id");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) fail(LKG_ERR_NCCL, "ncclGetUniqueId failed");
+    std::memcpy(id_out, id.internal, 128);
+  });
+}
+
+lkg_status lkg_ctx_init_nccl(lkg_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(id, "id");
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(LKG_ERR_INVALID_ARG, "bad rank/nranks");
+    DeviceGuard g(ctx->device);
+    ncclUniqueId uid;
+    std::memcpy(uid.internal, id, 128);
+    ncclComm_t comm;
+    const ncclResult_t r = ncclCommInitRank(&comm, nranks, uid, rank);
+    if (r != ncclSuccess) fail(LKG_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    if (ctx->nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl));
+    ctx->nccl = comm;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+  });
+}
+
+lkg_status lkg_model_forward_sharded(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n, const float* X,
+                                     int64_t rows, float* Y, lkg_oob_stats* stats) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    check_chain(chain, n);
+    if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
+    const int G = ctx->nranks;
+    if (G > 1 && !ctx->nccl) fail(LKG_ERR_NCCL, "context has no NCCL communicator");
+    for (int l = 0; l < n; l++) {
+      if (chain[l]->out_dim * G != chain[l]->full_out_dim)
+        fail(LKG_ERR_DIMENSION, "column shards must split out_dim evenly across ranks");
+      if (l > 0 && chain[l]->in_dim != chain[l - 1]->full_out_dim)
+        fail(LKG_ERR_DIMENSION, "artifact chain dimension mismatch between layers " + std::to_string(l - 1) +
+                                    " and " + std::to_string(l));
+    }
+    DeviceGuard g(ctx->device);
+    size_t loc = 0, full = 0;
+    for (int l = 0; l + 1 < n; l++) {
+      loc = std::max(loc, (size_t)chain[l]->out_dim);
+      full = std::max(full, (size_t)chain[l]->full_out_dim);
+    }
+    if (n > 1) {
+      ensure(ctx->scratch[0], sizeof(float) * rows * loc);
+      ensure(ctx->gather, sizeof(float) * rows * full);
+    }
+    const float* cur = X;
+    int32_t blk = 0;
+    for (int l = 0; l < n; l++) {
+      const bool last = l == n - 1;
+      float* dst = last ? Y : ctx->scratch[0].as<float>();
+      lkg::launch_forward(ctx, chain[l], cur, rows, blk, dst, l, true);
+      ctx->rows_seen[l] += (uint64_t)rows;
+      ctx->in_dim_seen[l] = chain[l]->in_dim;
+      if (!last) {
+        const size_t cnt = (size_t)rows * chain[l]->out_dim;
+        if (G > 1) {
+          const ncclResult_t r = ncclAllGather(dst, ctx->gather.p, cnt, ncclFloat, static_cast<ncclComm_t>(ctx->nccl),
+                                               ctx->stream);
+          if (r != ncclSuccess) fail(LKG_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+        } else {
+          LKG_CUDA(cudaMemcpyAsync(ctx->gather.p, dst, sizeof(float) * cnt, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        cur = ctx->gather.as<float>();
+        blk = chain[l]->out_dim;  // rank-major blocks of the gathered activations
+      }
+    }
+    if (stats) collect_impl(ctx, stats, n);
+  });
+}
+
+// ------------------------------------------------------------------ recipes
+lkg_status lkg_recipe_dims(int32_t cfg, int32_t* n_layers, int32_t* dims, int32_t* G, double* lo, double* hi) {
+  return guarded([&] {
+    need(n_layers, "n_layers");
+    need(dims, "dims");
+    int nl = 0, g = 0, d[5];
+    double a = 0, b = 0;
+    lkg::recipe_dims(cfg, &nl, d, &g, &a, &b);
+    *n_layers = nl;
+    for (int i = 0; i <= nl; i++) dims[i] = d[i];
+    if (G) *G = g;
+    if (lo) *lo = a;
+    if (hi) *hi = b;
+  });
+}
+
+lkg_status lkg_recipe_layer(int32_t cfg, int32_t layer, int32_t col0, int32_t col1, double* bp, double* coeffs,
+                            double* bs, double* ss, double* os) {
+  return guarded([&] {
+    need(bp, "breakpoints");
+    need(coeffs, "coeffs");
+    need(bs, "base_scale");
+    need(ss, "spline_scale");
+    need(os, "out_scale");
+    lkg::recipe_layer(cfg, layer, col0, col1, bp, coeffs, bs, ss, os);
+  });
+}
+
+lkg_status lkg_recipe_inputs(int32_t cfg, int64_t row0, int64_t rows, float* X) {
+  return guarded([&] {
+    if (rows > 0) need(X, "X");
+    if (row0 < 0 || rows < 0) fail(LKG_ERR_DIMENSION, "negative row range");
+    lkg::recipe_inputs(cfg, row0, rows, X);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,141 @@
+// lkg_internal.h — internal types of liblutkan_b200.so (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/lutkan_b200.h"
+
+namespace lkg {
+
+// Thread-local last error (lkg_last_error).
+void set_error(const std::string& msg);
+
+struct Error {
+  lkg_status code;
+  std::string msg;
+};
+
+#define LKG_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::lkg::Error{e_ == cudaErrorMemoryAllocation ? LKG_ERR_OOM : LKG_ERR_CUDA,   \
+                         std::string(#call) + ": " + cudaGetErrorString(e_)};            \
+  } while (0)
+
+// Device buffer owned by a layer/spec/context.
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void alloc(size_t n) {
+    release();
+    if (n) LKG_CUDA(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// Forward-kernel tile geometry chosen at upload time (forward.cu).
+struct TileGeom {
+  int32_t JB = 0;       // output columns per j-block (codes per lane-load)
+  int32_t IC = 0;       // inputs interleaved per 128-byte line
+  int32_t n_jb = 0;     // number of j-blocks
+  int32_t n_ic = 0;     // number of i-tiles
+  int64_t tile_bytes = 0;  // bytes of one (i-tile, j-block) tile, 128-aligned
+  int32_t p_off = 0, q_off = 0, cb_off = 0;  // byte offsets inside a tile
+  int32_t p_stride = 0;  // bytes between (k, i_lo) rows of the P block
+};
+
+}  // namespace lkg
+
+// Device artifact. The reference-layout arrays are kept for download/parity; the
+// forward kernels read the tiled copy built by lkg::build_tiles (forward.cu).
+struct lkg_layer {
+  int device = 0;
+  int32_t in_dim = 0, out_dim = 0, K = 0, L = 0;
+  int32_t col0 = 0, col1 = 0, full_out_dim = 0;  // column shard [col0, col1) of full_out_dim
+  int32_t value_repr = 1, scheme = 0, param_dtype = 0, boundary_mode = 1, oob_policy = 0;
+  std::vector<float> knots;  // host copy (K+1), fp32
+  lkg::DBuf q, scale, ymin, gains;  // reference layout: q [E,K,L], scale/ymin [E,K], gains [3][E]
+  lkg::DBuf float_table;            // optional [E,K,L] f64
+  lkg::DBuf cbcs;                   // fused gains fp32 [2][E]: cb = out*base, cs = out*spline
+  lkg::TileGeom geom;
+  lkg::DBuf tiles;                  // forward layout
+  uint64_t device_bytes() const {
+    return q.bytes + scale.bytes + ymin.bytes + gains.bytes + float_table.bytes + cbcs.bytes +
+           tiles.bytes;
+  }
+};
+
+struct lkg_spec {
+  int device = 0;
+  int32_t in_dim = 0, out_dim = 0, K = 0, degree = 3;
+  int32_t col0 = 0, col1 = 0, full_out_dim = 0;
+  std::vector<double> breakpoints;  // host f64 [K+1]
+  lkg::DBuf coeffs;    // f64 [E,R] (compile)
+  lkg::DBuf gains;     // f64 [3][E] base, spline, out (compile)
+  lkg::DBuf coeffs32;  // f32 [i][R][j] transposed for the spline forward
+  lkg::DBuf gains32;   // f32 [2][E]: out*base, out*spline
+};
+
+struct lkg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  uint64_t launches = 0;
+  // Per-layer-slot counters: [slot][4] = {n_oob_samples, n_oob_inputs, nonfinite, rows}.
+  static constexpr int kSlots = 64;
+  lkg::DBuf counters;
+  uint64_t rows_seen[kSlots] = {};
+  int32_t in_dim_seen[kSlots] = {};
+  lkg::DBuf scratch[2];  // hidden activations ping-pong
+  lkg::DBuf gather;      // sharded chain: all-gathered hidden activations
+  lkg::DBuf hostio;      // device staging for lkg_model_forward_host
+  void* nccl = nullptr;  // ncclComm_t
+  int32_t nranks = 1, rank = 0;
+};
+
+namespace lkg {
+
+// Kernel launch wrappers (forward.cu / compile.cu / spline.cu).
+void build_tiles(lkg_ctx* ctx, lkg_layer* L);
+// One layer forward. X has row stride x_ld and, when x_blk > 0, is stored as rank-major
+// column blocks of width x_blk (the NCCL all-gather layout): element (r, i) lives at
+// X[(i / x_blk) * rows * x_blk + r * x_blk + i % x_blk]. Y [rows, out_cols] row-major.
+void launch_forward(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk,
+                    float* Y, int slot, bool count_oob);
+void launch_compile(lkg_ctx* ctx, const lkg_spec* S, const lkg_quant_config* qc, lkg_layer* out,
+                    const double* d_basis, const int32_t* d_r0, const double* d_silu, int32_t W,
+                    bool keep_float);
+void launch_spline(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows, float* Y,
+                   const float* d_ext);
+void launch_fuse_gains(lkg_ctx* ctx, lkg_layer* L);
+void launch_coords(lkg_ctx* ctx, const lkg_layer* L, const float* x, int64_t n, int32_t* in_range, int32_t* k,
+                   int32_t* l0);
+void launch_spec_prepare(lkg_ctx* ctx, lkg_spec* S);
+
+// Host model_gen (model_gen.cpp).
+int recipe_dims(int cfg, int* n_layers, int* dims, int* G, double* lo, double* hi);
+void recipe_layer(int cfg, int layer, int col0, int col1, double* bp, double* coeffs, double* bs,
+                  double* ss, double* os);
+void recipe_inputs(int cfg, int64_t row0, int64_t rows, float* X);
+
+// Host Cox-de Boor (bit-exact restatement of spline.cpp:8-27,69-83) for compile tables.
+void knot_grid(const std::vector<double>& bp, int degree, std::vector<double>& ext);
+void basis_into(const std::vector<double>& T, int degree, double x, double* buf);
+double silu_host(double x);
+
+}  // namespace lkg

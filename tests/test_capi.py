@@ -1,0 +1,89 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol the public
+header declares (and the ctypes binding covers them), host-only entry points (synthetic
+config recipes) agree with the oracle, host-side validation mirrors the reference error
+taxonomy, and GPU calls fail loudly (no CPU fallback) on a machine without a GPU."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared(header):
+    txt = open(os.path.join(ROOT, "include", header)).read()
+    return sorted(set(re.findall(r"\b(lkg_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol(lk):
+    from paper_2601_03332_b200 import _capi
+    lib = _capi.lib()
+    declared = _declared("lutkan_b200.h")
+    assert len(declared) >= 25
+    nm = subprocess.run(["nm", "-D", "--defined-only", _capi.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (lkg_\w+)", nm))
+    missing = [s for s in declared if s not in exported]
+    assert not missing, missing
+    for s in declared:
+        assert getattr(lib, s) is not None
+        assert s in _capi.SIGNATURES, f"ctypes binding lacks {s}"
+
+
+def test_library_is_sm100a(lk):
+    from paper_2601_03332_b200 import _capi
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _capi.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_recipes_match_oracle(lk, oracle):
+    for cfg in (1, 2, 3):
+        dims, G, lo, hi = lk.recipe_dims(cfg)
+        for layer in range(len(dims) - 1):
+            s, o = lk.recipe_layer(cfg, layer), oracle.recipe_layer(cfg, layer)
+            assert np.array_equal(s.coeffs, o.coeffs) and np.array_equal(s.base_scale, o.base_scale)
+            assert np.array_equal(s.grid.breakpoints, o.breakpoints)
+        assert np.array_equal(lk.recipe_inputs(cfg, 3, 40), oracle.recipe_inputs(cfg, 3, 40))
+    # column shards are the matching slices of the full spec
+    full = lk.recipe_layer(3, 0)
+    part = lk.recipe_layer(3, 0, 10, 20)
+    assert np.array_equal(part.coeffs, full.coeffs.reshape(64, 64, -1)[:, 10:20].reshape(640, -1))
+    assert lk.recipe_dims(4)[0] == [1024, 1024, 1024, 10] and lk.recipe_dims(5)[0] == [4096, 4096, 4096]
+
+
+def test_recipe_errors(lk):
+    with pytest.raises(lk.ConfigError):
+        lk.recipe_dims(9)
+    with pytest.raises(lk.DimensionError):
+        lk.recipe_layer(1, 5)
+
+
+def test_enum_parsing_and_host_validation(lk):
+    assert lk.parse_enum("boundary_mode", "half_open") == lk.BoundaryMode.HalfOpen
+    with pytest.raises(lk.ConfigError):
+        lk.parse_enum("oob_policy", "wrap")
+    with pytest.raises(lk.ConfigError):
+        lk.QuantConfig(1).validate()
+    with pytest.raises(lk.ConfigError):
+        lk.QuantConfig(64, lk.Scheme.Symmetric, lk.Dtype.Uint8).validate()
+    a = lk.LutLayerArtifact(1, 1, 4, lk.ValueRepr.Phi, lk.Scheme.Asymmetric, lk.Dtype.Uint8, knots=np.array([0, 1, 2], np.float32),
+                            q_table=np.zeros(7, np.uint8), scale=np.ones(2, np.float32), y_min=np.zeros(2, np.float32))
+    with pytest.raises(lk.DimensionError):
+        a._desc()
+    st = lk.OobStats(3, 2, 6, 3)
+    st.merge(lk.OobStats(3, 2, 6, 3))
+    assert (st.n_samples, st.n_oob_inputs, st.oob_any_frac()) == (6, 6, pytest.approx(2 / 3))
+
+
+def test_gpu_calls_fail_loudly_without_gpu(lk):
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+    except ImportError:
+        pass
+    with pytest.raises(lk.CudaError):
+        lk.Engine(0)

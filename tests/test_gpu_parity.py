@@ -1,0 +1,281 @@
+"""GPU parity through the C-ABI (liblutkan_b200.so) against the CPU oracle.
+
+Bars (BASELINE.json north_star): LUT bytes / scales / y_mins, segment indices, OOB masks,
+OOB counts and argmax classes bit-exact; float outputs within max-abs 1e-5 (relative
+1e-5 where |y| > 1), per layer on identical fp32 inputs (the compiled table
+is discontinuous at knots, so chains are compared per layer plus argmax).
+"""
+import numpy as np
+import pytest
+
+from helpers import assert_close, hidden_inputs, stats_list, to_oracle_spec, to_product_artifact, to_product_spec
+from kat import HAND_CLOSED_CLIPX, HAND_CLOSED_ZS, hand_artifact_arrays
+
+pytestmark = pytest.mark.gpu
+
+
+def _bytes_equal(a, b):
+    return np.array_equal(np.asarray(a).view(np.uint8), np.asarray(b).view(np.uint8))
+
+
+def _compile_both(lk, oracle, cfg, layer, L, scheme, vr=1, pd=0, bm=1, op=0, keep_float=False):
+    spec = lk.recipe_layer(cfg, layer)
+    qc = lk.QuantConfig(L, lk.Scheme(scheme), lk.Dtype(scheme), lk.ValueRepr(vr), lk.Interp.Linear, lk.ParamDtype(pd))
+    oob = lk.OobConfig(lk.BoundaryMode(bm), lk.OobPolicy(op))
+    g = lk.compile_layer_debug_float(spec, qc, oob) if keep_float else lk.compile_layer(spec, qc, oob)
+    o = oracle.compile_layer(to_oracle_spec(spec), L, scheme, vr, pd, bm, op, keep_float=keep_float)
+    return spec, g, o
+
+
+# ------------------------------------------------------------------ compile
+@pytest.mark.parametrize("cfg,layer,L,scheme", [(1, 0, 64, 0), (1, 1, 64, 0), (2, 0, 64, 0), (2, 0, 64, 1),
+                                                (2, 1, 64, 1), (3, 0, 16, 0), (3, 0, 32, 1), (3, 0, 64, 0),
+                                                (3, 0, 128, 1), (3, 1, 128, 0)])
+def test_compile_bit_exact(lk, oracle, cfg, layer, L, scheme):
+    _, g, o = _compile_both(lk, oracle, cfg, layer, L, scheme)
+    assert _bytes_equal(g.q_table, o.q)
+    assert _bytes_equal(g.scale, o.scale) and _bytes_equal(g.y_min, o.y_min)
+    assert _bytes_equal(g.knots, o.knots)
+    for a, b in ((g.edge_base_scale, o.base_scale), (g.edge_spline_scale, o.spline_scale), (g.edge_out_scale, o.out_scale)):
+        assert _bytes_equal(a, b)
+
+
+@pytest.mark.parametrize("vr,pd", [(0, 0), (0, 1), (1, 1)])
+def test_compile_phi_and_f16_bit_exact(lk, oracle, vr, pd):
+    for scheme in (0, 1):
+        _, g, o = _compile_both(lk, oracle, 2, 0, 32, scheme, vr, pd, keep_float=True)
+        assert _bytes_equal(g.q_table, o.q) and _bytes_equal(g.scale, o.scale) and _bytes_equal(g.y_min, o.y_min)
+        assert _bytes_equal(g.float_table, o.float_table)
+        if vr == 0:
+            assert g.edge_base_scale is None and g.base_kind == ""
+
+
+def test_compile_large_edge_slices(lk, oracle):
+    """C4 (1024x1024, K=8, L=64) compiled whole on the GPU; the oracle compiles per-input-row
+    edge slices, which are exactly the matching byte ranges."""
+    spec = lk.recipe_layer(4, 0)
+    g = lk.compile_layer(spec, lk.QuantConfig(64), lk.OobConfig(lk.BoundaryMode.HalfOpen, lk.OobPolicy.ClipX))
+    os_ = to_oracle_spec(spec)
+    m, K, L = 1024, 8, 64
+    for i in (0, 1, 511, 1023):
+        o = oracle.compile_layer(os_.edge_slice(i, i + 1), 64, 0, 1, 0, 0, 0)
+        assert _bytes_equal(g.q_table[i * m * K * L:(i + 1) * m * K * L], o.q)
+        assert _bytes_equal(g.scale[i * m * K:(i + 1) * m * K], o.scale)
+
+
+def test_compile_c5_column_shard(lk, oracle):
+    """C5 geometry (G=16 on [-2,2], L=128, uint8 asym): a column shard compiled on the GPU
+    matches the oracle's compile of the same edges."""
+    cols = (1024, 1088)
+    spec = lk.recipe_layer(5, 0, *cols)
+    g = lk.compile_layer(spec, lk.QuantConfig(128, lk.Scheme.Asymmetric, lk.Dtype.Uint8),
+                         lk.OobConfig(lk.BoundaryMode.Closed, lk.OobPolicy.ZeroSpline))
+    mc, K, L = cols[1] - cols[0], 16, 128
+    for i in (0, 4095):
+        o = oracle.compile_layer(to_oracle_spec(spec).edge_slice(i, i + 1), 128, 1, 1, 0, 1, 1)
+        assert _bytes_equal(g.q_table[i * mc * K * L:(i + 1) * mc * K * L], o.q)
+        assert _bytes_equal(g.y_min[i * mc * K:(i + 1) * mc * K], o.y_min)
+
+
+# ------------------------------------------------------------------ coordinates
+@pytest.mark.parametrize("bm", [0, 1])
+def test_segment_index_and_mask_bit_exact(lk, oracle, engine, bm):
+    import ctypes as C
+    import torch
+    from paper_2601_03332_b200._capi import lib
+    for cfg in (3, 5):
+        spec = lk.recipe_layer(cfg, 0, 0, 1)
+        g = lk.compile_layer(spec, lk.QuantConfig(128 if cfg == 5 else 16),
+                             lk.OobConfig(lk.BoundaryMode(bm), lk.OobPolicy.ZeroSpline))
+        knots = g.knots
+        adv = [knots, np.nextafter(knots, np.float32(np.inf)), np.nextafter(knots, np.float32(-np.inf))]
+        rng = np.random.default_rng(5)
+        x = np.concatenate(adv + [rng.uniform(knots[0] * 1.3, knots[-1] * 1.3, 200000).astype(np.float32)])
+        x = x.astype(np.float32)
+        xd = torch.from_numpy(x).cuda()
+        ind, kd, l0d = (torch.zeros(len(x), dtype=torch.int32, device="cuda") for _ in range(3))
+        dl = g.device(engine)
+        torch.cuda.synchronize()
+        lk.lutkan.check(lib().lkg_layer_coords(engine.handle, dl.handle, C.c_void_p(xd.data_ptr()), len(x),
+                                               C.c_void_p(ind.data_ptr()), C.c_void_p(kd.data_ptr()),
+                                               C.c_void_p(l0d.data_ptr())))
+        from oracle.pyoracle import Artifact
+        oa = Artifact(1, 1, g.L, g.knots, g.q_table, g.scale, g.y_min, g.edge_base_scale, g.edge_spline_scale,
+                      g.edge_out_scale, 1, 0, 0, bm, 1)
+        c = oracle.coords(oa, x.astype(np.float64))
+        assert np.array_equal(ind.cpu().numpy().astype(bool), c["in_range"])
+        assert np.array_equal(kd.cpu().numpy(), c["k"])
+        l0_mis = np.mean(l0d.cpu().numpy() != c["l0"])
+        assert l0_mis == 0.0, l0_mis
+
+
+# ------------------------------------------------------------------ forward
+def _layer_parity(lk, oracle, art_o, X, what):
+    a = to_product_artifact(lk, art_o)
+    Y, st = lk.lut_layer_forward_batch(a, X)
+    Yo, sto = oracle.lut_forward(art_o, X.astype(np.float64))
+    err = assert_close(Y, Yo, what)
+    assert stats_list(st) == [int(v) for v in sto], what
+    return err
+
+
+@pytest.mark.parametrize("cfg,rows", [(1, 4096), (2, 20000)])
+def test_forward_layers_c1_c2(lk, oracle, cfg, rows):
+    for scheme in (0, 1):
+        contract = (0, 0) if cfg == 1 else (1, 0)
+        for layer in (0, 1):
+            spec = oracle.recipe_layer(cfg, layer)
+            art = oracle.compile_layer(spec, 64, scheme, 1, 0, *contract)
+            X = oracle.recipe_inputs(cfg, 0, rows) if layer == 0 else hidden_inputs(cfg, layer, rows, spec.in_dim)
+            _layer_parity(lk, oracle, art, X, f"C{cfg} layer {layer} scheme {scheme}")
+
+
+@pytest.mark.parametrize("L", [16, 32, 64, 128])
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_forward_c3_cells(lk, oracle, L, scheme):
+    """All 32 cells of C3's resolution x quantization x OOB sweep (layer 0, 64->64)."""
+    spec = oracle.recipe_layer(3, 0)
+    X = oracle.recipe_inputs(3, 0, 4096)
+    for bm in (0, 1):
+        for op in (0, 1):
+            art = oracle.compile_layer(spec, L, scheme, 1, 0, bm, op)
+            _layer_parity(lk, oracle, art, X, f"C3 L{L} s{scheme} bm{bm} op{op}")
+
+
+def test_forward_phi_and_float_table(lk, oracle):
+    spec = oracle.recipe_layer(2, 0)
+    X = oracle.recipe_inputs(2, 0, 3000)
+    for op in (0, 1):
+        art = oracle.compile_layer(spec, 32, 1, 0, 0, 0, op)
+        _layer_parity(lk, oracle, art, X, f"phi op{op}")
+        art = oracle.compile_layer(spec, 32, 0, 1, 0, 0, op, keep_float=True)
+        _layer_parity(lk, oracle, art, X, f"float_table op{op}")
+
+
+def test_forward_c4_layer_rows(lk, oracle):
+    spec = oracle.recipe_layer(4, 0)
+    art = oracle.compile_layer(spec, 64, 0, 1, 0, 0, 0)
+    X = oracle.recipe_inputs(4, 0, 48)
+    _layer_parity(lk, oracle, art, X, "C4 layer 0")
+    spec = oracle.recipe_layer(4, 2)   # 1024 -> 10
+    art = oracle.compile_layer(spec, 64, 0, 1, 0, 0, 0)
+    _layer_parity(lk, oracle, art, hidden_inputs(4, 2, 512, 1024), "C4 layer 2")
+
+
+def test_forward_c5_column_shard(lk, oracle):
+    """C5 contract (L=128 uint8 asym, closed, zero_spline, d=4096): a column shard."""
+    cols = (0, 48)
+    spec = lk.recipe_layer(5, 0, *cols)
+    art = oracle.compile_layer(to_oracle_spec(spec), 128, 1, 1, 0, 1, 1)
+    X = lk.recipe_inputs(5, 0, 24)
+    _layer_parity(lk, oracle, art, X, "C5 shard")
+
+
+def test_chain_argmax_c2(lk, oracle):
+    """C2 end to end: argmax classes of the GPU chain vs the f64 oracle chain."""
+    rows = 50000
+    X = oracle.recipe_inputs(2, 0, rows)
+    for scheme in (0, 1):
+        chain_o = [oracle.compile_layer(oracle.recipe_layer(2, l), 64, scheme, 1, 0, 1, 0) for l in range(2)]
+        r = lk.lut_model_forward_batch([to_product_artifact(lk, a) for a in chain_o], X)
+        Yo, sto = oracle.lut_model_forward(chain_o, X.astype(np.float64))
+        agree = np.argmax(r.Y, 1) == np.argmax(Yo, 1)
+        # any disagreement must be a near-tie of the two logits
+        gap = np.abs(Yo[:, 0] - Yo[:, 1])
+        assert np.all(agree | (gap < 1e-4)), (np.sum(~agree), gap[~agree].max())
+        assert [stats_list(s) for s in r.per_layer] == sto.astype(int).tolist()
+
+
+def test_chain_c1(lk, oracle):
+    X = oracle.recipe_inputs(1, 0, 4096)
+    chain_o = [oracle.compile_layer(oracle.recipe_layer(1, l), 64, 0, 1, 0, 0, 0) for l in range(2)]
+    chain = [to_product_artifact(lk, a) for a in chain_o]
+    r = lk.lut_model_forward_batch(chain, X)
+    # per-layer parity on the GPU's own hidden activations
+    H, _ = lk.lut_layer_forward_batch(chain[0], X)
+    _layer_parity(lk, oracle, chain_o[1], H, "C1 layer 1 on GPU hidden")
+    Y2, _ = lk.lut_layer_forward_batch(chain[1], H)
+    assert np.array_equal(r.Y, Y2)
+
+
+# ------------------------------------------------------------------ spline
+@pytest.mark.parametrize("cfg,layer,rows", [(1, 0, 4096), (2, 0, 4000), (3, 0, 2000), (4, 2, 256)])
+def test_spline_forward(lk, oracle, cfg, layer, rows):
+    spec = lk.recipe_layer(cfg, layer)
+    X = oracle.recipe_inputs(cfg, 0, rows) if layer == 0 else hidden_inputs(cfg, layer, rows, spec.in_dim, -2.5, 2.5)
+    Y = lk.layer_forward_batch(spec, X)
+    Yo = oracle.spline_forward(to_oracle_spec(spec), X.astype(np.float64))
+    assert_close(Y, Yo, f"spline C{cfg}")
+
+
+# ------------------------------------------------------------------ KATs / errors
+def _hand(lk, bm, op):
+    h = hand_artifact_arrays(bm, op)
+    return lk.LutLayerArtifact(1, 1, 4, lk.ValueRepr.Phi, lk.Scheme.Asymmetric, lk.Dtype.Uint8, lk.ParamDtype.F32,
+                               lk.OobConfig(lk.BoundaryMode(bm), lk.OobPolicy(op)), "",
+                               knots=h["knots"], q_table=h["q"], scale=h["scale"], y_min=h["y_min"])
+
+
+def test_kat_hand_table_gpu(lk):
+    a = _hand(lk, 1, 0)
+    xs = np.array([[x] for x, _, _ in HAND_CLOSED_CLIPX], np.float32)
+    Y, st = lk.lut_layer_forward_batch(a, xs)
+    assert np.allclose(Y[:, 0], [v for _, v, _ in HAND_CLOSED_CLIPX], rtol=1e-6, atol=0)
+    assert st.n_oob_inputs == sum(o for _, _, o in HAND_CLOSED_CLIPX)
+    Y, _ = lk.lut_layer_forward_batch(a, np.array([[0.0], [1.0], [2.0]], np.float32))
+    assert Y[:, 0].tolist() == [0.0, 40.0, 70.0]    # segment starts are exact
+    a = _hand(lk, 1, 1)
+    Y, _ = lk.lut_layer_forward_batch(a, np.array([[x] for x, _, _ in HAND_CLOSED_ZS], np.float32))
+    assert Y[:, 0].tolist() == [v for _, v, _ in HAND_CLOSED_ZS]
+    a = _hand(lk, 0, 1)    # half_open masks the top knot
+    Y, st = lk.lut_layer_forward_batch(a, np.array([[2.0], [1.9999]], np.float32))
+    assert Y[0, 0] == 0.0 and st.n_oob_inputs == 1
+
+
+def test_oob_stats_gpu(lk, oracle):
+    spec = oracle.recipe_layer(1, 0)
+    art = oracle.compile_layer(spec, 8, 0, 1, 0, 0, 0)
+    a = to_product_artifact(lk, art)
+    tK = float(spec.breakpoints[-1])
+    X = np.array([[0.0, 0.0], [tK, 0.0], [tK, tK + 5.0]], np.float32)
+    _, st = lk.lut_layer_forward_batch(a, X)
+    assert stats_list(st) == [3, 2, 6, 3]
+    assert st.oob_any_frac() == pytest.approx(2 / 3)
+
+
+def test_errors_and_edges_gpu(lk, oracle):
+    a = _hand(lk, 1, 0)
+    with pytest.raises(lk.NonFiniteError):
+        lk.lut_layer_forward_batch(a, np.array([[np.nan]], np.float32))
+    with pytest.raises(lk.NonFiniteError):
+        lk.lut_layer_forward_batch(a, np.array([[0.5], [-np.inf]], np.float32))
+    Y, st = lk.lut_layer_forward_batch(a, np.array([[0.5]], np.float32))   # context recovers after an error
+    assert Y[0, 0] == pytest.approx(15.0)
+    with pytest.raises(lk.DimensionError):
+        lk.lut_layer_forward_batch(a, np.zeros((2, 3), np.float32))
+    with pytest.raises(lk.ConfigError):
+        lk.lut_model_forward_batch([], np.zeros((1, 1), np.float32))
+    spec = oracle.recipe_layer(1, 0)
+    art = to_product_artifact(lk, oracle.compile_layer(spec, 8, 0, 1, 0, 0, 0))
+    with pytest.raises(lk.DimensionError):
+        lk.lut_model_forward_batch([art, art], np.zeros((1, 2), np.float32))
+    Y, st = lk.lut_layer_forward_batch(art, np.zeros((0, 2), np.float32))     # empty batch
+    assert Y.shape == (0, 5) and stats_list(st) == [0, 0, 0, 0]
+    bad = _hand(lk, 1, 0)
+    bad.dtype = lk.Dtype.Int8       # asymmetric requires uint8 (runtime.cpp:21-22)
+    with pytest.raises(lk.ConfigError):
+        bad.finalize()
+    bad = _hand(lk, 1, 0)
+    bad.knots = np.array([0, 2, 1], np.float32)
+    with pytest.raises(lk.ConfigError):
+        bad.finalize()
+    bad = _hand(lk, 1, 0)
+    bad.scale = np.ones(3, np.float32)
+    with pytest.raises(lk.DimensionError):
+        bad.finalize()
+    s = lk.recipe_layer(1, 0)
+    s.base_kind = "tanh"
+    with pytest.raises(lk.UnsupportedBaseError):
+        lk.layer_forward_batch(s, np.zeros((1, 2), np.float32))
+    with pytest.raises(lk.ConfigError):
+        lk.compile_layer(lk.recipe_layer(1, 0), lk.QuantConfig(1))
