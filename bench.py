@@ -176,7 +176,8 @@ def main():
     dims, G, _, _ = lk.recipe_dims(cfg)
     nl = len(dims) - 1
     ee_row = sum(dims[l] * dims[l + 1] for l in range(nl))
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=local)   # the engine runs on this stream; events are recorded on it
+    torch.cuda.set_stream(stream)
     eng = lk.Engine(local, stream.cuda_stream)
     qc = lk.QuantConfig(L, lk.Scheme(scheme), lk.Dtype(scheme))
     oob = lk.OobConfig(lk.BoundaryMode(bm), lk.OobPolicy(op))

@@ -44,7 +44,7 @@ def build(verbose: bool = False) -> str:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
     if not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", LIB, *objs, "-lnccl"]
+        cmd = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", LIB, *objs, "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -16,6 +16,42 @@
 
 #include "lkg_internal.h"
 
+// NCCL is resolved lazily with dlopen, and only by the column-shard entry points: the
+// process may already hold another libnccl.so.2 (PyTorch bundles its own), and linking
+// one at load time would shadow it. RTLD_NOLOAD first reuses whatever is loaded.
+#include <dlfcn.h>
+namespace {
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw lkg::Error{LKG_ERR_NCCL, std::string("cannot load libnccl.so.2: ") + dlerror()};
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (!a.GetUniqueId || !a.CommInitRank || !a.CommDestroy || !a.AllGather || !a.GetErrorString)
+      throw lkg::Error{LKG_ERR_NCCL, "libnccl.so.2 lacks a required symbol"};
+    return a;
+  }();
+  return api;
+}
+}  // namespace
+#define ncclGetUniqueId nccl_api().GetUniqueId
+#define ncclCommInitRank nccl_api().CommInitRank
+#define ncclCommDestroy nccl_api().CommDestroy
+#define ncclAllGather nccl_api().AllGather
+#define ncclGetErrorString nccl_api().GetErrorString
+
 namespace lkg {
 namespace {
 thread_local std::string g_err;

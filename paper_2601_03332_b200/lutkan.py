@@ -191,7 +191,9 @@ class Engine:
 
     def __init__(self, device: int = 0, stream: int | None = None):
         h = C.c_void_p()
-        check(lib().lkg_ctx_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
+        # None -> private stream; 0 (the legacy default stream) -> cudaStreamLegacy (0x1)
+        s = None if stream is None else C.c_void_p(stream if stream != 0 else 1)
+        check(lib().lkg_ctx_create(device, s, C.byref(h)))
         self.handle, self.device = h, device
 
     def close(self):
