@@ -182,7 +182,6 @@ void launch_fuse_gains(lkg_ctx* ctx, lkg_layer* L) {
   ctx->launches++;
 }
 
-void build_tiles(lkg_ctx*, lkg_layer*) {}
 
 static FwdArgs layer_args(const lkg_layer* L) {
   if (L->K > kMaxK) throw Error{LKG_ERR_CONFIG, "segment count above kernel limit"};
@@ -211,6 +210,10 @@ void launch_coords(lkg_ctx* ctx, const lkg_layer* L, const float* x, int64_t n, 
 void launch_forward(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk,
                     float* Y, int slot, bool count_oob) {
   if (rows <= 0) return;
+  if (tiled_eligible(L)) {
+    launch_forward_tiled(ctx, L, X, rows, x_blk, Y, slot);
+    return;
+  }
   FwdArgs a = layer_args(L);
   a.X = X;
   a.rows = rows;

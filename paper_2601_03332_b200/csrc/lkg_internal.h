@@ -53,7 +53,7 @@ struct TileGeom {
   int32_t JB = 0;       // output columns per j-block (codes per lane-load)
   int32_t IC = 0;       // inputs interleaved per 128-byte line
   int32_t n_jb = 0;     // number of j-blocks
-  int32_t n_ic = 0;     // number of i-tiles
+  int32_t n_ih = 0;     // number of i-tiles
   int64_t tile_bytes = 0;  // bytes of one (i-tile, j-block) tile, 128-aligned
   int32_t p_off = 0, q_off = 0, cb_off = 0;  // byte offsets inside a tile
   int32_t p_stride = 0;  // bytes between (k, i_lo) rows of the P block
@@ -112,6 +112,9 @@ namespace lkg {
 
 // Kernel launch wrappers (forward.cu / compile.cu / spline.cu).
 void build_tiles(lkg_ctx* ctx, lkg_layer* L);
+bool tiled_eligible(const lkg_layer* L);
+void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk, float* Y,
+                          int slot);
 // One layer forward. X has row stride x_ld and, when x_blk > 0, is stored as rank-major
 // column blocks of width x_blk (the NCCL all-gather layout): element (r, i) lives at
 // X[(i / x_blk) * rows * x_blk + r * x_blk + i % x_blk]. Y [rows, out_cols] row-major.
