@@ -545,6 +545,18 @@ static void run_chain(lkg_ctx* ctx, const lkg_layer* const* chain, int n, const 
   const float* cur = X;
   for (int l = 0; l < n; l++) {
     float* dst = l == n - 1 ? Y : ctx->scratch[l & 1].as<float>();
+    if (l + 1 < n && rows > 0 && lkg::can_fuse(chain[l], chain[l + 1])) {
+      // layer l and the small layer l+1 in one launch; the hidden activations never leave registers
+      float* dst2 = l + 1 == n - 1 ? Y : ctx->scratch[(l + 1) & 1].as<float>();
+      lkg::launch_forward_tiled(ctx, chain[l], cur, rows, 0, nullptr, l, chain[l + 1], dst2);
+      for (int s = l; s <= l + 1; s++) {
+        ctx->rows_seen[s] += (uint64_t)rows;
+        ctx->in_dim_seen[s] = chain[s]->in_dim;
+      }
+      cur = dst2;
+      l++;
+      continue;
+    }
     lkg::launch_forward(ctx, chain[l], cur, rows, 0, dst, l, true);
     ctx->rows_seen[l] += (uint64_t)rows;
     ctx->in_dim_seen[l] = chain[l]->in_dim;

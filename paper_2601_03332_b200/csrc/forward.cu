@@ -87,6 +87,24 @@ __global__ void coords_kernel(FwdArgs a, const float* x, int64_t n, int32_t* in_
   if (l0) l0[t] = c.l0;
 }
 
+struct CoordArgs {
+  lkg::CoordConst cc;
+  float4 ktab[lkg::kMaxKT];
+};
+
+__global__ void coords_tiled_kernel(const __grid_constant__ CoordArgs c, const float* x, int64_t n,
+                                    int32_t* in_range, int32_t* k, int32_t* l0) {
+  __shared__ float4 ktab[lkg::kMaxKT];
+  for (int q = threadIdx.x; q < c.cc.K; q += blockDim.x) ktab[q] = c.ktab[q];
+  __syncthreads();
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const lkg::Coord co = lkg::lut_coords(c.cc, ktab, x[t]);
+  if (in_range) in_range[t] = co.in;
+  if (k) k[t] = co.k;
+  if (l0) l0[t] = co.l0;
+}
+
 template <bool SR, bool ZS, bool I8, bool FT>
 __global__ void __launch_bounds__(kThreads) fwd_simple(FwdArgs a) {
   // coordinate scratch for RB rows x JT inputs
@@ -199,6 +217,14 @@ static FwdArgs layer_args(const lkg_layer* L) {
 void launch_coords(lkg_ctx* ctx, const lkg_layer* L, const float* x, int64_t n, int32_t* in_range, int32_t* k,
                    int32_t* l0) {
   if (n <= 0) return;
+  if (L->geom.tile_bytes > 0) {  // the tiled / small kernels' coordinate path (coords.cuh)
+    CoordArgs c{};
+    fill_coord_const(L, c.cc, c.ktab);
+    coords_tiled_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(c, x, n, in_range, k, l0);
+    LKG_CUDA(cudaGetLastError());
+    ctx->launches++;
+    return;
+  }
   FwdArgs a = layer_args(L);
   const unsigned g = (unsigned)((n + 255) / 256);
   if (L->oob_policy == LKG_OOB_ZERO_SPLINE) coords_kernel<true><<<g, 256, 0, ctx->stream>>>(a, x, n, in_range, k, l0);

@@ -31,17 +31,20 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
+#include "coords.cuh"
 #include "lkg_internal.h"
 
 namespace {
 
+using lkg::kMaxKT;
 constexpr int G = 8;                // inputs per line
 constexpr int JB = 16;              // outputs per line / j-block
 constexpr int LINE = G * JB;        // 128 bytes
 constexpr int PROW = 80;            // bytes per P/Q/CB row (16 floats + 16 B pad, conflict-free)
-constexpr int kMaxKT = 64;
 constexpr int kFlushBlocks = 8;     // f64 flush every 8 tiles = 64 inputs
 constexpr int kFp32MaxD = 256;      // fp32 accumulation bound
 
@@ -52,15 +55,21 @@ struct TiledArgs {
   int32_t p_off, q_off, cb_off;
   const float* X;
   int64_t rows;
-  int32_t d, x_blk;
+  int32_t d, x_blk, x_vec2;  // x_vec2: even row stride and 8-aligned column blocks -> float2 loads
   float* Y;
   int32_t m;
   unsigned long long* counters;
-  int32_t K, L;
-  float lo, hi, hi_clip, est_scale;
-  int32_t half_open;
+  lkg::CoordConst cc;        // coordinate constants (coords.cuh)
   int64_t n_items;
   float4 ktab[kMaxKT];  // {T_k, T_k+1, (L-1)/(T_k+1 - T_k), 0}
+  // fused next layer (FUSE): a small-out_dim layer evaluated in the epilogue from the 16 hidden
+  // activations each lane holds (the whole-layer "small" layout, resident in shared memory)
+  const uint8_t* lut2;
+  int32_t lut2_bytes, p_off2, q_off2, cb_off2, MP2, m2;
+  float* Y2;
+  unsigned long long* counters2;
+  lkg::CoordConst cc2;
+  float4 ktab2[kMaxKT];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -96,30 +105,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-__device__ __forceinline__ float load_x(const TiledArgs& a, int64_t r, int i) {
-  if (a.x_blk <= 0) return __ldg(a.X + r * a.d + i);
-  const int b = i / a.x_blk;
-  return __ldg(a.X + (int64_t)b * a.rows * a.x_blk + r * a.x_blk + (i - b * a.x_blk));
-}
-
 __device__ __forceinline__ float magic(uint32_t w, uint32_t sel) {
   return __uint_as_float(__byte_perm(w, 0x4B000000u, sel));  // 2^23 + byte
 }
 
-template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64>
+template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE>
 __global__ void __launch_bounds__(W * 32, 1) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int NS = 2;
   constexpr int ROWS_W = 32 * R;        // rows per warp
   constexpr int XS = ROWS_W + 4;        // padded row stride of the transposed x tile
+  constexpr int NX = 4 * R;             // float2 x loads per lane per tile
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t tb = a.tile_bytes;
-  uint8_t* stage = smem;                                             // NS * tile_bytes
+  uint8_t* stage = smem;                                                  // NS * tile_bytes
   float* xs = reinterpret_cast<float*>(smem + NS * tb) + warp * G * XS;  // per-warp x tile
   float4* ktab = reinterpret_cast<float4*>(smem + NS * tb + W * G * XS * 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + kMaxKT);
+  float4* ktab2 = reinterpret_cast<float4*>(full + 4);
+  uint8_t* lut2 = reinterpret_cast<uint8_t*>(ktab2 + kMaxKT);
 
-  for (int k = tid; k < a.K; k += W * 32) ktab[k] = a.ktab[k];
+  for (int k = tid; k < a.cc.K; k += W * 32) ktab[k] = a.ktab[k];
+  if (FUSE) {
+    for (int k = tid; k < a.cc2.K; k += W * 32) ktab2[k] = a.ktab2[k];
+    for (int o = tid * 16; o < a.lut2_bytes; o += W * 32 * 16)
+      *reinterpret_cast<uint4*>(lut2 + o) = __ldg(reinterpret_cast<const uint4*>(a.lut2 + o));
+  }
   if (tid == 0) {
     for (int s = 0; s < NS; s++) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -128,14 +139,11 @@ __global__ void __launch_bounds__(W * 32, 1) fwd_tiled(const __grid_constant__ T
 
   const int64_t n_local = a.n_items > blockIdx.x ? (a.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t n_stages = n_local * a.n_ih;
-  auto tile_src = [&](int64_t g) {
+  auto issue = [&](int64_t g) {
     const int64_t item = blockIdx.x + (g / a.n_ih) * gridDim.x;
     const int jb = (int)(item % a.n_jb), ih = (int)(g % a.n_ih);
-    return a.tiles + ((int64_t)jb * a.n_ih + ih) * tb;
-  };
-  auto issue = [&](int64_t g) {
+    const uint8_t* src = a.tiles + ((int64_t)jb * a.n_ih + ih) * tb;
     uint8_t* dst = stage + (g % NS) * tb;
-    const uint8_t* src = tile_src(g);
     mbar_expect_tx(&full[g % NS], (uint32_t)tb);
     for (int64_t off = 0; off < tb; off += 32768) {
       const uint32_t n = (uint32_t)(tb - off < 32768 ? tb - off : 32768);
@@ -147,58 +155,82 @@ __global__ void __launch_bounds__(W * 32, 1) fwd_tiled(const __grid_constant__ T
 
   const float M = 8388608.0f;  // 2^23
   const float OFF = ASYM ? 0.0f : 128.0f;
-  unsigned long long oob_inputs = 0, oob_rows = 0;
-  bool nonfinite = false;
+  const float lo = a.cc.lo;
+  const int K = a.cc.K, L = a.cc.L;  // knots are uniformly spaced (tiled_eligible)
+  uint32_t oob_inputs = 0, oob_rows = 0, oob2_inputs = 0, oob2_rows = 0;
+  bool nonfinite = false, nonfinite2 = false;
   int64_t g = 0;
+  // x staging coordinates of this lane: rows lane/4 + 8t, columns 2*(lane&3) + {0,1}
+  const int xr_row = lane >> 2, xr_col = 2 * (lane & 3);
+  const int64_t x_rs = a.x_blk > 0 ? a.x_blk : a.d;  // row stride of the input layout
 
   for (int64_t li = 0; li < n_local; li++) {
     const int64_t item = blockIdx.x + li * gridDim.x;
     const int64_t rt = item / a.n_jb;
     const int jb = (int)(item % a.n_jb);
-    const bool count = jb == 0;
+    const int cnt = jb == 0;  // OOB statistics are counted once per row (j-block 0)
     const int64_t row0 = rt * (int64_t)(W * ROWS_W) + warp * ROWS_W;
+    const int64_t rows_left = a.rows - row0;  // rows of this warp: [0, min(ROWS_W, rows_left))
     float2 acc[R][8];
     double acc64[F64 ? R : 1][F64 ? 16 : 1];
-    bool row_oob[R];
+    uint32_t row_oob = 0;  // bit r: row lane + 32 r saw an OOB coordinate
 #pragma unroll
     for (int r = 0; r < R; r++) {
-      row_oob[r] = false;
 #pragma unroll
       for (int q = 0; q < 8; q++) acc[r][q] = make_float2(0.f, 0.f);
       if (F64)
 #pragma unroll
         for (int q = 0; q < 16; q++) acc64[r][q] = 0.0;
     }
-    // prefetch x for tile 0 into registers
-    float xr[R * G];
-#define LOAD_XBLOCK(IH)                                             \
-  _Pragma("unroll") for (int t = 0; t < R * G; t++) {               \
-    const int e = t * 32 + lane, rr = e >> 3, c = e & 7;            \
-    const int64_t row = row0 + rr;                                  \
-    const int i = (IH) * G + c;                                     \
-    xr[t] = (row < a.rows && i < a.d) ? load_x(a, row, i) : 0.0f;   \
+    float2 xr[NX];
+    // x tile (rows row0.., columns 8*ih..8*ih+7) into registers. Cells outside [rows) x [d) read
+    // as t_0: finite and in range, so they never count as OOB; their P and CB entries are 0.
+#define LOAD_XBLOCK(IH)                                                                   \
+  {                                                                                       \
+    const int i_ = (IH) * G + xr_col;                                                     \
+    int64_t cb_;                                                                          \
+    if (a.x_blk > 0) {                                                                    \
+      const int b_ = ((IH) * G) / a.x_blk;                                                \
+      cb_ = (int64_t)b_ * a.rows * a.x_blk + ((IH) * G - b_ * a.x_blk) + xr_col;           \
+    } else {                                                                              \
+      cb_ = (int64_t)(IH) * G + xr_col;                                                   \
+    }                                                                                     \
+    const float* p_ = a.X + cb_ + (row0 + xr_row) * x_rs;                                 \
+    const bool c0_ = i_ < a.d, c1_ = i_ + 1 < a.d;                                        \
+    _Pragma("unroll") for (int t = 0; t < NX; t++) {                                      \
+      float2 v_ = make_float2(lo, lo);                                                    \
+      if (xr_row + 8 * t < rows_left) {                                                   \
+        const float* q_ = p_ + (int64_t)(8 * t) * x_rs;                                   \
+        if (a.x_vec2 && c1_) {                                                            \
+          v_ = __ldg(reinterpret_cast<const float2*>(q_));                                \
+        } else {                                                                          \
+          if (c0_) v_.x = __ldg(q_);                                                      \
+          if (c1_) v_.y = __ldg(q_ + 1);                                                  \
+        }                                                                                 \
+      }                                                                                   \
+      xr[t] = v_;                                                                         \
+    }                                                                                     \
   }
     LOAD_XBLOCK(0);
 
     for (int ih = 0; ih < a.n_ih; ih++, g++) {
-      // stage this warp's x tile transposed: xs[c][row] (conflict-free, see DESIGN.md §4)
+      // stage this warp's x tile transposed: xs[c][row] (conflict-free, DESIGN.md §4)
       __syncwarp();
 #pragma unroll
-      for (int t = 0; t < R * G; t++) {
-        const int e = t * 32 + lane;
-        xs[(e & 7) * XS + (e >> 3)] = xr[t];
+      for (int t = 0; t < NX; t++) {
+        xs[xr_col * XS + xr_row + 8 * t] = xr[t].x;
+        xs[(xr_col + 1) * XS + xr_row + 8 * t] = xr[t].y;
       }
       __syncwarp();
-      if (ih + 1 < a.n_ih) {
-        LOAD_XBLOCK(ih + 1);
-      }
+      if (ih + 1 < a.n_ih) LOAD_XBLOCK(ih + 1);
       mbar_wait(&full[g % NS], (uint32_t)((g / NS) & 1));
       const uint8_t* T = stage + (g % NS) * tb;
 
 #pragma unroll 1
       for (int s = 0; s < G; s++) {
         const int il = (s + lane) & 7;
-        const int i = ih * G + il;
+        const uint8_t* Tq = T + il * JB;
+        const uint8_t* Tp = T + a.p_off + il * PROW;
         float2 cb[8];
         if (SR) {
           const float4* cbp = reinterpret_cast<const float4*>(T + a.cb_off + il * PROW);
@@ -212,45 +244,21 @@ __global__ void __launch_bounds__(W * 32, 1) fwd_tiled(const __grid_constant__ T
 #pragma unroll
         for (int r = 0; r < R; r++) {
           const float x = xs[il * XS + lane + 32 * r];
-          // ---- steps 1-4: mask, clip, segment, interpolation coordinates
-          const bool valid_i = i < a.d;
-          const bool in = a.lo <= x && (a.half_open ? x < a.hi : x <= a.hi);
-          if (valid_i) {
-            nonfinite |= !isfinite(x);
-            if (count && row0 + lane + 32 * r < a.rows && !in) {
-              oob_inputs++;
-              row_oob[r] = true;
-            }
-          }
-          const float xp = fminf(fmaxf(x, a.lo), a.hi_clip);
-          int k = (int)((xp - a.lo) * a.est_scale);
-          k = k < 0 ? 0 : (k > a.K - 1 ? a.K - 1 : k);
-          float4 kt = ktab[k];
-          while (k > 0 && xp < kt.x) kt = ktab[--k];
-          while (k < a.K - 1 && xp >= kt.y) kt = ktab[++k];
-          const float z = (xp - kt.x) * kt.z;
-          float fl = floorf(z);
-          float w1 = z - fl;
-          int l0 = (int)fl;
-          if (w1 < 0x1p-12f || w1 > 1.0f - 0x1p-12f || l0 >= a.L - 1 || l0 < 0) {
-            // near a sample node: runtime.cpp:178-181 in f64
-            const double u = ((double)xp - (double)kt.x) / ((double)kt.y - (double)kt.x);
-            const double zz = u * (double)(a.L - 1);
-            int ll = (int)floor(zz);
-            ll = ll < 0 ? 0 : (ll > a.L - 1 ? a.L - 1 : ll);
-            l0 = ll;
-            w1 = (float)(zz - (double)ll);
-          }
-          if (l0 >= a.L - 1) w1 = 0.0f;
-          w1 = (w1 + 1.0f) - 1.0f;  // multiple of 2^-23: keeps the magic constants exact
+          // ---- steps 1-4 (runtime.cpp:170-190): mask, clip, segment, coordinates (coords.cuh)
+          const lkg::Coord co = lkg::lut_coords(a.cc, ktab, x);
+          const bool in = co.in;
+          const int k = co.k, l0 = co.l0;
+          const float xp = co.xp, w1 = co.w1;  // w1: multiple of 2^-23 -> exact magic constants
+          nonfinite |= !(fabsf(x) <= 3.402823466e38f);
+          oob_inputs += (uint32_t)(cnt & !in);
+          row_oob |= (uint32_t)(!in) << r;
           const float w0 = 1.0f - w1;
           const float cA = -fmaf(w0, M, OFF), cB = -w1 * M;
-          const bool masked = ZS && !in;
-          const uint8_t* qp = T + (k * a.L + l0) * LINE + il * JB;
+          const uint8_t* qp = Tq + (k * L + l0) * LINE;
           const uint4 c0 = *reinterpret_cast<const uint4*>(qp);
           const uint4 c1 = *reinterpret_cast<const uint4*>(qp + LINE);
-          const int prow = (masked ? a.K : k) * G + il;
-          const float4* pp = reinterpret_cast<const float4*>(T + a.p_off + prow * PROW);
+          const int prow = ((ZS && !in) ? K : k) * (G * PROW);  // zero block masks the table term
+          const float4* pp = reinterpret_cast<const float4*>(Tp + prow);
           float bx = 0.0f;
           if (SR) {
             const float xb = ZS ? x : xp;  // clip_x clips the base branch too (runtime.cpp:189)
@@ -279,7 +287,7 @@ __global__ void __launch_bounds__(W * 32, 1) fwd_tiled(const __grid_constant__ T
               s1 = __ffma2_rn(cb[2 * q + 1], BX, s1);
             }
             if (ASYM) {
-              const float4 Q = reinterpret_cast<const float4*>(T + a.q_off + prow * PROW)[q];
+              const float4 Q = reinterpret_cast<const float4*>(T + a.q_off + il * PROW + prow)[q];
               s0 = __fadd2_rn(s0, make_float2(Q.x, Q.y));
               s1 = __fadd2_rn(s1, make_float2(Q.z, Q.w));
             }
@@ -301,40 +309,239 @@ __global__ void __launch_bounds__(W * 32, 1) fwd_tiled(const __grid_constant__ T
       __syncthreads();  // every warp is done with this stage buffer
       if (tid == 0 && g + NS < n_stages) issue(g + NS);
     }
+#undef LOAD_XBLOCK
     // epilogue: rows of this lane, 16 outputs of the j-block
     const int j0 = jb * JB;
 #pragma unroll
     for (int r = 0; r < R; r++) {
       const int64_t row = row0 + lane + 32 * r;
-      if (row < a.rows) {
+      if (lane + 32 * r < rows_left) {
         float out[16];
 #pragma unroll
         for (int q = 0; q < 8; q++) {
           out[2 * q] = F64 ? (float)acc64[r][2 * q] : acc[r][q].x;
           out[2 * q + 1] = F64 ? (float)acc64[r][2 * q + 1] : acc[r][q].y;
         }
-        float* yr = a.Y + row * a.m + j0;
-        if (j0 + 16 <= a.m && (a.m & 3) == 0) {
+        if (FUSE) {
+          // next layer (runtime.cpp:298-314 chain) on this row's hidden activations out[0..m)
+          const int K2 = a.cc2.K, L2 = a.cc2.L, MP2 = a.MP2;
+          const float* P2 = reinterpret_cast<const float*>(lut2 + a.p_off2);
+          const float* Q2 = reinterpret_cast<const float*>(lut2 + a.q_off2);
+          const float* CB2 = reinterpret_cast<const float*>(lut2 + a.cb_off2);
+          float y2[8];
 #pragma unroll
-          for (int q = 0; q < 4; q++)
-            reinterpret_cast<float4*>(yr)[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+          for (int j = 0; j < 8; j++) y2[j] = 0.0f;
+          bool r_oob2 = false;
+#pragma unroll
+          for (int i2 = 0; i2 < 16; i2++) {
+            if (i2 < a.m) {
+              const float h = out[i2];
+              const lkg::Coord c2 = lkg::lut_coords(a.cc2, ktab2, h);
+              nonfinite2 |= !(fabsf(h) <= 3.402823466e38f);
+              oob2_inputs += (uint32_t)!c2.in;
+              r_oob2 |= !c2.in;
+              const bool tab = !(ZS && !c2.in);
+              float bx2 = 0.0f;
+              if (SR) {
+                const float xb = ZS ? h : c2.xp;
+                bx2 = __fdividef(xb, 1.0f + __expf(-xb));
+              }
+              const int cell = i2 * K2 + c2.k, l1 = min(c2.l0 + 1, L2 - 1);
+              const uint8_t* q0p = lut2 + (cell * L2 + c2.l0) * MP2;
+              const uint8_t* q1p = lut2 + (cell * L2 + l1) * MP2;
+              const float w1 = c2.w1, w0 = 1.0f - w1;
+#pragma unroll
+              for (int j = 0; j < 8; j++) {
+                if (j < a.m2) {
+                  const float q0 = ASYM ? (float)q0p[j] : (float)(int8_t)q0p[j];
+                  const float q1 = ASYM ? (float)q1p[j] : (float)(int8_t)q1p[j];
+                  float v = 0.0f;
+                  if (tab) {
+                    v = P2[cell * MP2 + j] * fmaf(w1, q1, w0 * q0);
+                    if (ASYM) v += Q2[cell * MP2 + j];
+                  }
+                  y2[j] += SR ? fmaf(CB2[i2 * MP2 + j], bx2, v) : v;
+                }
+              }
+            }
+          }
+          float* y2r = a.Y2 + row * a.m2;
+#pragma unroll
+          for (int j = 0; j < 8; j++)
+            if (j < a.m2) y2r[j] = y2[j];
+          oob2_rows += (uint32_t)r_oob2;
         } else {
-          for (int q = 0; q < 16 && j0 + q < a.m; q++) yr[q] = out[q];
+          float* yr = a.Y + row * a.m + j0;
+          if (j0 + 16 <= a.m && (a.m & 3) == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              reinterpret_cast<float4*>(yr)[q] = make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; q++)
+              if (j0 + q < a.m) yr[q] = out[q];
+          }
         }
-        if (row_oob[r]) oob_rows++;
+        oob_rows += (uint32_t)(cnt & (row_oob >> r));
       }
     }
   }
   // OOB counters (runtime.cpp:216-222) and the non-finite flag (runtime.cpp:172)
+  unsigned long long oi = oob_inputs, orow = oob_rows;
   for (int o = 16; o; o >>= 1) {
-    oob_inputs += __shfl_xor_sync(0xffffffffu, oob_inputs, o);
-    oob_rows += __shfl_xor_sync(0xffffffffu, oob_rows, o);
+    oi += __shfl_xor_sync(0xffffffffu, oi, o);
+    orow += __shfl_xor_sync(0xffffffffu, orow, o);
   }
   if (lane == 0) {
-    if (oob_rows) atomicAdd(a.counters + 0, oob_rows);
-    if (oob_inputs) atomicAdd(a.counters + 1, oob_inputs);
+    if (orow) atomicAdd(a.counters + 0, orow);
+    if (oi) atomicAdd(a.counters + 1, oi);
   }
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicExch(a.counters + 2, 1ull);
+  if (FUSE) {
+    unsigned long long oi2 = oob2_inputs, orow2 = oob2_rows;
+    for (int o = 16; o; o >>= 1) {
+      oi2 += __shfl_xor_sync(0xffffffffu, oi2, o);
+      orow2 += __shfl_xor_sync(0xffffffffu, orow2, o);
+    }
+    if (lane == 0) {
+      if (orow2) atomicAdd(a.counters2 + 0, orow2);
+      if (oi2) atomicAdd(a.counters2 + 1, oi2);
+    }
+    if (__any_sync(0xffffffffu, nonfinite2) && lane == 0) atomicExch(a.counters2 + 2, 1ull);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Small-out_dim layers (m <= 8, whole LUT <= ~200 KB, d <= 256): the entire layer is resident
+// in shared memory; lanes are (row, input) pairs and each row's partial sums are reduced over
+// its input lanes with butterfly shuffles. Layout: codes [d][K][L][MP] (MP = m rounded up to
+// 1/2/4/8 bytes), P = out*spline*scale [d][K][MP] f32, Q = out*spline*y_min, CB [d][MP].
+struct SmallArgs {
+  const uint8_t* lut;
+  int32_t lut_bytes, p_off, q_off, cb_off, MP;
+  const float* X;
+  int64_t rows;
+  int32_t d, x_blk;
+  float* Y;
+  int32_t m;
+  unsigned long long* counters;
+  lkg::CoordConst cc;
+  float4 ktab[kMaxKT];
+};
+
+template <bool ASYM, bool SR, bool ZS>
+__global__ void __launch_bounds__(256) fwd_small(const __grid_constant__ SmallArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* lut = smem;
+  float4* ktab = reinterpret_cast<float4*>(smem + ((a.lut_bytes + 15) & ~15));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = blockDim.x >> 5;
+  for (int o = tid * 16; o < a.lut_bytes; o += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(lut + o) = __ldg(reinterpret_cast<const uint4*>(a.lut + o));
+  for (int k = tid; k < a.cc.K; k += blockDim.x) ktab[k] = a.ktab[k];
+  __syncthreads();
+  int DP = 1;
+  while (DP < a.d && DP < 32) DP <<= 1;
+  const int RPW = 32 / DP, li = lane & (DP - 1), rsub = lane / DP;
+  const float lo = a.cc.lo;
+  const int K = a.cc.K, L = a.cc.L, MP = a.MP, m = a.m;
+  const int64_t x_rs = a.x_blk > 0 ? a.x_blk : a.d;
+  uint32_t oob_inputs = 0, oob_rows = 0;
+  bool nonfinite = false;
+  const int64_t step = (int64_t)gridDim.x * W * RPW;
+  for (int64_t rbase = ((int64_t)blockIdx.x * W + warp) * RPW; rbase < a.rows; rbase += step) {
+    const int64_t row = rbase + rsub;
+    const bool vrow = row < a.rows;
+    float part[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) part[j] = 0.0f;
+    bool any_oob = false;
+    for (int i = li; i < a.d; i += DP) {
+      float x = lo;
+      if (vrow) {
+        int64_t off;
+        if (a.x_blk > 0) {
+          const int b = i / a.x_blk;
+          off = (int64_t)b * a.rows * a.x_blk + row * x_rs + (i - b * a.x_blk);
+        } else {
+          off = row * x_rs + i;
+        }
+        x = __ldg(a.X + off);
+      }
+      const lkg::Coord co = lkg::lut_coords(a.cc, ktab, x);
+      const bool in = co.in;
+      const int k = co.k, l0 = co.l0;
+      const float xp = co.xp, w1 = co.w1;
+      nonfinite |= !(fabsf(x) <= 3.402823466e38f);
+      oob_inputs += (uint32_t)!in;
+      any_oob |= !in;
+      const int l1 = min(l0 + 1, L - 1);
+      const float w0 = 1.0f - w1;
+      const uint8_t* c0 = lut + ((i * K + k) * L + l0) * MP;
+      const uint8_t* c1 = lut + ((i * K + k) * L + l1) * MP;
+      const float* P = reinterpret_cast<const float*>(lut + a.p_off) + (i * K + k) * MP;
+      const float* Q = reinterpret_cast<const float*>(lut + a.q_off) + (i * K + k) * MP;
+      const float* CB = reinterpret_cast<const float*>(lut + a.cb_off) + i * MP;
+      const bool tab = !(ZS && !in);
+      float bx = 0.0f;
+      if (SR) {
+        const float xb = ZS ? x : xp;
+        bx = __fdividef(xb, 1.0f + __expf(-xb));
+      }
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        if (j < m) {
+          const float q0 = ASYM ? (float)c0[j] : (float)(int8_t)c0[j];
+          const float q1 = ASYM ? (float)c1[j] : (float)(int8_t)c1[j];
+          float v = 0.0f;
+          if (tab) {
+            v = P[j] * fmaf(w1, q1, w0 * q0);
+            if (ASYM) v += Q[j];
+          }
+          part[j] += SR ? fmaf(CB[j], bx, v) : v;
+        }
+      }
+    }
+    // reduce over the DP input lanes of each row
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+      if (j < m)
+        for (int o = 1; o < DP; o <<= 1) part[j] += __shfl_xor_sync(0xffffffffu, part[j], o);
+    for (int o = 1; o < DP; o <<= 1) any_oob |= __shfl_xor_sync(0xffffffffu, (int)any_oob, o) != 0;
+    if (vrow && li == 0) {
+      float* yr = a.Y + row * m;
+#pragma unroll
+      for (int j = 0; j < 8; j++)
+        if (j < m) yr[j] = part[j];
+      oob_rows += any_oob;
+    }
+  }
+  unsigned long long oi = oob_inputs, orow = oob_rows;
+  for (int o = 16; o; o >>= 1) {
+    oi += __shfl_xor_sync(0xffffffffu, oi, o);
+    orow += __shfl_xor_sync(0xffffffffu, orow, o);
+  }
+  if (lane == 0) {
+    if (orow) atomicAdd(a.counters + 0, orow);
+    if (oi) atomicAdd(a.counters + 1, oi);
+  }
+  if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicExch(a.counters + 2, 1ull);
+}
+
+__global__ void build_small_kernel(const uint8_t* q, const float* scale, const float* ymin, const float* gains,
+                                   uint8_t* lut, int32_t d, int32_t m, int32_t K, int32_t L, int32_t MP,
+                                   int32_t p_off, int32_t q_off, int32_t cb_off, int sr, int asym) {
+  const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t E = (int64_t)d * m;
+  if (cell >= E * K) return;
+  const int64_t e = cell / K;
+  const int k = (int)(cell - e * K);
+  const int i = (int)(e / m), j = (int)(e - (int64_t)i * m);
+  for (int l = 0; l < L; l++) lut[((int64_t)(i * K + k) * L + l) * MP + j] = q[cell * L + l];
+  const double cs = sr ? (double)gains[2 * E + e] * (double)gains[E + e] : 1.0;
+  reinterpret_cast<float*>(lut + p_off)[(i * K + k) * MP + j] = (float)(cs * (double)scale[cell]);
+  if (asym) reinterpret_cast<float*>(lut + q_off)[(i * K + k) * MP + j] = (float)(cs * (double)ymin[cell]);
+  if (sr && k == 0)
+    reinterpret_cast<float*>(lut + cb_off)[i * MP + j] = (float)((double)gains[2 * E + e] * (double)gains[e]);
 }
 
 // Reference layout -> tiles (one thread per (edge, segment) cell).
@@ -361,9 +568,9 @@ __global__ void build_tiles_kernel(const uint8_t* q, const float* scale, const f
     *reinterpret_cast<float*>(t + cb_off + il * PROW + jl * 4) = (float)((double)gains[2 * E + e] * (double)gains[e]);
 }
 
-template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64>
+template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false>
 void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
-  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64>;
+  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE>;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -378,6 +585,7 @@ namespace lkg {
 
 static constexpr int kW = 16, kR = 2;          // fp32 mode: 16 warps x 64 rows = 1024-row tiles
 static constexpr int kW64 = 8, kR64 = 2;       // f64-flush mode: 8 warps x 64 rows = 512-row tiles
+static constexpr int kSmallMaxBytes = 200 * 1024;
 
 bool tiled_eligible(const lkg_layer* L) {
   if (L->float_table.p || L->K > kMaxKT) return false;
@@ -388,8 +596,42 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   TileGeom& gm = L->geom;
   gm = TileGeom{};
   if (L->float_table.p || L->K > kMaxKT) return;
+  {  // the in-kernel segment estimate needs uniformly spaced knots (all BASELINE grids are)
+    double hmin = 1e300, hmax = 0;
+    for (int k = 0; k < L->K; k++) {
+      hmin = std::min(hmin, (double)L->knots[k + 1] - L->knots[k]);
+      hmax = std::max(hmax, (double)L->knots[k + 1] - L->knots[k]);
+    }
+    if (hmax > hmin * (1.0 + 1e-4)) return;
+  }
   const int d = L->in_dim, m = L->col1 - L->col0, K = L->K, Ls = L->L;
   const bool asym = L->scheme == LKG_SCHEME_ASYMMETRIC, sr = L->value_repr == LKG_REPR_SPLINE_COMPONENT;
+  const int64_t cells = (int64_t)d * m * K;
+  // small out_dim: the whole layer in shared memory (fwd_small)
+  if (m <= 8 && d <= kFp32MaxD) {
+    const int MP = m <= 1 ? 1 : (m <= 2 ? 2 : (m <= 4 ? 4 : 8));
+    int64_t off = ((int64_t)d * K * Ls * MP + 15) / 16 * 16;
+    const int64_t pq = ((int64_t)d * K * MP * 4 + 15) / 16 * 16;
+    gm.p_off = (int32_t)off;
+    off += pq;
+    gm.q_off = (int32_t)off;
+    if (asym) off += pq;
+    gm.cb_off = (int32_t)off;
+    off += ((int64_t)d * MP * 4 + 15) / 16 * 16;
+    if (off + kMaxKT * 16 <= kSmallMaxBytes) {
+      gm.small = 1;
+      gm.MP = MP;
+      gm.tile_bytes = off;
+      L->tiles.alloc((size_t)off);
+      LKG_CUDA(cudaMemsetAsync(L->tiles.p, 0, L->tiles.bytes, ctx->stream));
+      build_small_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(
+          L->q.as<uint8_t>(), L->scale.as<float>(), L->ymin.as<float>(), L->gains.as<float>(), L->tiles.as<uint8_t>(),
+          d, m, K, Ls, MP, gm.p_off, gm.q_off, gm.cb_off, sr, asym);
+      LKG_CUDA(cudaGetLastError());
+      ctx->launches++;
+      return;
+    }
+  }
   int64_t off = (int64_t)(K * Ls + 1) * LINE;
   gm.p_off = (int32_t)off;
   off += (int64_t)(K + 1) * G * PROW;
@@ -403,7 +645,7 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   }
   off = (off + 127) / 128 * 128;
   const size_t xs_bytes = (size_t)kW * G * (32 * kR + 4) * 4;
-  if (2 * off + xs_bytes + kMaxKT * 16 + 64 > 227 * 1024) return;  // tile too large: generic kernel
+  if (2 * off + xs_bytes + kMaxKT * 16 + 32 > 227 * 1024) return;  // tile too large: generic kernel
   gm.tile_bytes = off;
   gm.JB = JB;
   gm.IC = G;
@@ -411,7 +653,6 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   gm.n_jb = (m + JB - 1) / JB;
   L->tiles.alloc((size_t)gm.n_ih * gm.n_jb * off);
   LKG_CUDA(cudaMemsetAsync(L->tiles.p, 0, L->tiles.bytes, ctx->stream));
-  const int64_t cells = (int64_t)d * m * K;
   build_tiles_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(
       L->q.as<uint8_t>(), L->scale.as<float>(), L->ymin.as<float>(), L->gains.as<float>(), L->tiles.as<uint8_t>(),
       off, gm.n_ih, d, m, K, Ls, gm.p_off, gm.q_off, gm.cb_off, !asym, sr, asym);
@@ -419,9 +660,107 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   ctx->launches++;
 }
 
-void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk, float* Y,
-                          int slot) {
+// Per-layer coordinate constants (coords.cuh), from the artifact's f32 knots.
+void fill_coord_const(const lkg_layer* L, CoordConst& c, float4* ktab) {
+  c.K = L->K;
+  c.L = L->L;
+  const bool half_open = L->boundary_mode == LKG_BOUNDARY_HALF_OPEN;
+  const float hi = L->knots[L->K];
+  c.lo = L->knots[0];
+  c.hi_clip = half_open ? std::nextafterf(hi, -INFINITY) : hi;  // runtime.cpp:150-153
+  c.inv_h = (float)L->K / (hi - c.lo);
+  for (int k = 0; k < L->K; k++) {
+    const float t0 = L->knots[k], t1 = L->knots[k + 1];
+    ktab[k] = make_float4(t0, t1, (float)(L->L - 1) / (t1 - t0), 0.f);
+  }
+  // fp32 z = (x' - t_k) * (L-1)/h carries <= 3 roundings: re-evaluate in f64 within 8x that of a node
+  c.z_thr = (float)std::max(8.0 * 0x1p-24 * (L->L - 1), 0x1p-20);
+  {  // x' == hi_clip, evaluated exactly as runtime.cpp:176-181
+    const double T0 = L->knots[L->K - 1], T1 = L->knots[L->K];
+    const double u = ((double)c.hi_clip - T0) / (T1 - T0), zz = u * (double)(L->L - 1);
+    int l0 = (int)std::floor(zz);
+    l0 = l0 < 0 ? 0 : (l0 > L->L - 1 ? L->L - 1 : l0);
+    c.top_l0 = l0;
+    c.top_w1 = (float)(zz - (double)l0);
+  }
+}
+
+static int sm_count(int dev) {
+  static int sms[64] = {0};
+  if (dev < 0 || dev >= 64) return 148;
+  if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  return sms[dev] > 0 ? sms[dev] : 148;
+}
+
+template <bool ASYM, bool SR, bool ZS>
+static void launch_small_t(cudaStream_t st, const SmallArgs& a, size_t smem, int grid) {
+  auto kern = fwd_small<ASYM, SR, ZS>;
+  static bool attr = false;
+  if (!attr) {
+    LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  kern<<<grid, 256, smem, st>>>(a);
+}
+
+static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk,
+                                 float* Y, int slot) {
   const TileGeom& gm = L->geom;
+  SmallArgs a{};
+  a.lut = L->tiles.as<uint8_t>();
+  a.lut_bytes = (int32_t)gm.tile_bytes;
+  a.p_off = gm.p_off;
+  a.q_off = gm.q_off;
+  a.cb_off = gm.cb_off;
+  a.MP = gm.MP;
+  a.X = X;
+  a.rows = rows;
+  a.d = L->in_dim;
+  a.x_blk = x_blk;
+  a.Y = Y;
+  a.m = L->col1 - L->col0;
+  a.counters = ctx->counters.as<unsigned long long>() + 4 * slot;
+  fill_coord_const(L, a.cc, a.ktab);
+  int DP = 1;
+  while (DP < a.d && DP < 32) DP <<= 1;
+  const int64_t groups = (rows + (32 / DP) * 8 - 1) / ((32 / DP) * 8);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(groups, 2 * sm_count(ctx->device)));
+  const size_t smem = ((gm.tile_bytes + 15) & ~15) + kMaxKT * 16;
+  const bool asym = L->scheme == LKG_SCHEME_ASYMMETRIC, sr = L->value_repr == LKG_REPR_SPLINE_COMPONENT;
+  const bool zs = L->oob_policy == LKG_OOB_ZERO_SPLINE;
+  switch ((asym << 2) | (sr << 1) | (int)zs) {
+    case 0: launch_small_t<false, false, false>(ctx->stream, a, smem, grid); break;
+    case 1: launch_small_t<false, false, true>(ctx->stream, a, smem, grid); break;
+    case 2: launch_small_t<false, true, false>(ctx->stream, a, smem, grid); break;
+    case 3: launch_small_t<false, true, true>(ctx->stream, a, smem, grid); break;
+    case 4: launch_small_t<true, false, false>(ctx->stream, a, smem, grid); break;
+    case 5: launch_small_t<true, false, true>(ctx->stream, a, smem, grid); break;
+    case 6: launch_small_t<true, true, false>(ctx->stream, a, smem, grid); break;
+    default: launch_small_t<true, true, true>(ctx->stream, a, smem, grid); break;
+  }
+  LKG_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
+static size_t tiled_smem(const lkg_layer* L, int W, int R) {
+  return 2 * L->geom.tile_bytes + (size_t)W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 32;
+}
+
+bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
+  const TileGeom &g1 = L1->geom, &g2 = L2->geom;
+  if (!g1.tile_bytes || g1.small || g1.n_jb != 1 || !g2.tile_bytes || !g2.small) return false;
+  if (L1->in_dim > kFp32MaxD || L2->in_dim != L1->col1 - L1->col0 || L2->col1 - L2->col0 > 8) return false;
+  if (L1->scheme != L2->scheme || L1->value_repr != L2->value_repr || L1->oob_policy != L2->oob_policy) return false;
+  return tiled_smem(L1, kW, kR) + kMaxKT * 16 + ((g2.tile_bytes + 15) & ~15) <= 227 * 1024;
+}
+
+void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk, float* Y,
+                          int slot, const lkg_layer* L2, float* Y2) {
+  const TileGeom& gm = L->geom;
+  if (gm.small) {
+    launch_forward_small(ctx, L, X, rows, x_blk, Y, slot);
+    return;
+  }
   TiledArgs a{};
   a.tiles = L->tiles.as<uint8_t>();
   a.tile_bytes = gm.tile_bytes;
@@ -437,38 +776,49 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   a.Y = Y;
   a.m = L->col1 - L->col0;
   a.counters = ctx->counters.as<unsigned long long>() + 4 * slot;
-  a.K = L->K;
-  a.L = L->L;
-  a.half_open = L->boundary_mode == LKG_BOUNDARY_HALF_OPEN;
-  a.lo = L->knots[0];
-  a.hi = L->knots[L->K];
-  a.hi_clip = a.half_open ? std::nextafterf(a.hi, -INFINITY) : a.hi;
-  a.est_scale = (float)L->K / (a.hi - a.lo);
-  for (int k = 0; k < L->K; k++) {
-    const float t0 = L->knots[k], t1 = L->knots[k + 1];
-    a.ktab[k] = make_float4(t0, t1, (float)(L->L - 1) / (t1 - t0), 0.f);
-  }
+  a.x_vec2 = (x_blk <= 0 ? (L->in_dim % 2 == 0) : (x_blk % 8 == 0));
+  fill_coord_const(L, a.cc, a.ktab);
   const bool f64 = L->in_dim > kFp32MaxD;
+  const bool asym = L->scheme == LKG_SCHEME_ASYMMETRIC, sr = L->value_repr == LKG_REPR_SPLINE_COMPONENT;
+  const bool zs = L->oob_policy == LKG_OOB_ZERO_SPLINE;
   const int W = f64 ? kW64 : kW, R = f64 ? kR64 : kR;
   const int64_t row_tile = (int64_t)W * 32 * R;
   a.n_items = ((rows + row_tile - 1) / row_tile) * gm.n_jb;
-  int dev = ctx->device, sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = (int)std::min<int64_t>(a.n_items, sms);
-  const size_t smem = 2 * gm.tile_bytes + (size_t)W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 64;
-  const bool asym = L->scheme == LKG_SCHEME_ASYMMETRIC, sr = L->value_repr == LKG_REPR_SPLINE_COMPONENT;
-  const bool zs = L->oob_policy == LKG_OOB_ZERO_SPLINE;
-  const int sel = (f64 << 3) | (asym << 2) | (sr << 1) | (int)zs;
+  const int grid = (int)std::min<int64_t>(a.n_items, sm_count(ctx->device));
+  size_t smem = tiled_smem(L, W, R);
+  const int sel = (asym << 2) | (sr << 1) | (int)zs;
+  if (L2) {  // fused chain step: this layer + the small next layer in one launch
+    const TileGeom& g2 = L2->geom;
+    a.lut2 = L2->tiles.as<uint8_t>();
+    a.lut2_bytes = (int32_t)g2.tile_bytes;
+    a.p_off2 = g2.p_off;
+    a.q_off2 = g2.q_off;
+    a.cb_off2 = g2.cb_off;
+    a.MP2 = g2.MP;
+    a.m2 = L2->col1 - L2->col0;
+    a.Y2 = Y2;
+    a.counters2 = ctx->counters.as<unsigned long long>() + 4 * (slot + 1);
+    fill_coord_const(L2, a.cc2, a.ktab2);
+    smem += kMaxKT * 16 + ((g2.tile_bytes + 15) & ~15);
+    switch (sel) {
+#define CASE(S) \
+  case S: launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, true>(ctx->stream, a, smem, grid); break;
+      CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+    }
+    LKG_CUDA(cudaGetLastError());
+    ctx->launches++;
+    return;
+  }
   switch (sel) {
-#define CASE(S)                                                                                           \
-  case S:                                                                                                 \
-    if ((S >> 3) & 1)                                                                                     \
-      launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true>(ctx->stream, a, smem, grid);     \
-    else                                                                                                  \
-      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false>(ctx->stream, a, smem, grid);        \
+#define CASE(S)                                                                                     \
+  case S:                                                                                           \
+    if (f64)                                                                                        \
+      launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true>(ctx->stream, a, smem, grid); \
+    else                                                                                            \
+      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false>(ctx->stream, a, smem, grid);    \
     break;
     CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
-    CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
 #undef CASE
   }
   LKG_CUDA(cudaGetLastError());

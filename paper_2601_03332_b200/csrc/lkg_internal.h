@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../../include/lutkan_b200.h"
+#include "coords.cuh"
 
 namespace lkg {
 
@@ -57,6 +58,7 @@ struct TileGeom {
   int64_t tile_bytes = 0;  // bytes of one (i-tile, j-block) tile, 128-aligned
   int32_t p_off = 0, q_off = 0, cb_off = 0;  // byte offsets inside a tile
   int32_t p_stride = 0;  // bytes between (k, i_lo) rows of the P block
+  int32_t small = 0, MP = 0;  // whole-layer-in-smem layout (m <= 8), MP = padded out_dim
 };
 
 }  // namespace lkg
@@ -113,8 +115,11 @@ namespace lkg {
 // Kernel launch wrappers (forward.cu / compile.cu / spline.cu).
 void build_tiles(lkg_ctx* ctx, lkg_layer* L);
 bool tiled_eligible(const lkg_layer* L);
+void fill_coord_const(const lkg_layer* L, CoordConst& c, float4* ktab);
 void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk, float* Y,
-                          int slot);
+                          int slot, const lkg_layer* L2 = nullptr, float* Y2 = nullptr);
+// True when layer L2 (small out_dim, whole LUT in smem) can run in L1's epilogue (chain fusion).
+bool can_fuse(const lkg_layer* L1, const lkg_layer* L2);
 // One layer forward. X has row stride x_ld and, when x_blk > 0, is stored as rank-major
 // column blocks of width x_blk (the NCCL all-gather layout): element (r, i) lives at
 // X[(i / x_blk) * rows * x_blk + r * x_blk + i % x_blk]. Y [rows, out_cols] row-major.

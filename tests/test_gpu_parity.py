@@ -184,6 +184,11 @@ def test_chain_argmax_c2(lk, oracle):
         gap = np.abs(Yo[:, 0] - Yo[:, 1])
         assert np.all(agree | (gap < 1e-4)), (np.sum(~agree), gap[~agree].max())
         assert [stats_list(s) for s in r.per_layer] == sto.astype(int).tolist()
+        # the chain (layer 2 fused into layer 1's epilogue) per layer on the GPU's own hidden values
+        chain = [to_product_artifact(lk, a) for a in chain_o]
+        H, _ = lk.lut_layer_forward_batch(chain[0], X[:5000])
+        Y2o, _ = oracle.lut_forward(chain_o[1], H.astype(np.float64))
+        assert_close(r.Y[:5000], Y2o, "C2 fused layer 2")
 
 
 def test_chain_c1(lk, oracle):
