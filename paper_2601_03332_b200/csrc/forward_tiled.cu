@@ -325,8 +325,6 @@ __global__ void __launch_bounds__(W * 32, 1) fwd_tiled(const __grid_constant__ T
         if (FUSE) {
           // next layer (runtime.cpp:298-314 chain) on this row's hidden activations out[0..m)
           const int K2 = a.cc2.K, L2 = a.cc2.L, MP2 = a.MP2;
-          const float* P2 = reinterpret_cast<const float*>(lut2 + a.p_off2);
-          const float* Q2 = reinterpret_cast<const float*>(lut2 + a.q_off2);
           const float* CB2 = reinterpret_cast<const float*>(lut2 + a.cb_off2);
           float y2[8];
 #pragma unroll
@@ -347,19 +345,13 @@ __global__ void __launch_bounds__(W * 32, 1) fwd_tiled(const __grid_constant__ T
                 bx2 = __fdividef(xb, 1.0f + __expf(-xb));
               }
               const int cell = i2 * K2 + c2.k, l1 = min(c2.l0 + 1, L2 - 1);
-              const uint8_t* q0p = lut2 + (cell * L2 + c2.l0) * MP2;
-              const uint8_t* q1p = lut2 + (cell * L2 + l1) * MP2;
+              const float* V0 = reinterpret_cast<const float*>(lut2) + (cell * L2 + c2.l0) * MP2;
+              const float* V1 = reinterpret_cast<const float*>(lut2) + (cell * L2 + l1) * MP2;
               const float w1 = c2.w1, w0 = 1.0f - w1;
 #pragma unroll
               for (int j = 0; j < 8; j++) {
                 if (j < a.m2) {
-                  const float q0 = ASYM ? (float)q0p[j] : (float)(int8_t)q0p[j];
-                  const float q1 = ASYM ? (float)q1p[j] : (float)(int8_t)q1p[j];
-                  float v = 0.0f;
-                  if (tab) {
-                    v = P2[cell * MP2 + j] * fmaf(w1, q1, w0 * q0);
-                    if (ASYM) v += Q2[cell * MP2 + j];
-                  }
+                  const float v = tab ? fmaf(w1, V1[j], w0 * V0[j]) : 0.0f;
                   y2[j] += SR ? fmaf(CB2[i2 * MP2 + j], bx2, v) : v;
                 }
               }
@@ -412,10 +404,12 @@ __global__ void __launch_bounds__(W * 32, 1) fwd_tiled(const __grid_constant__ T
 }
 
 // ---------------------------------------------------------------------------------------
-// Small-out_dim layers (m <= 8, whole LUT <= ~200 KB, d <= 256): the entire layer is resident
-// in shared memory; lanes are (row, input) pairs and each row's partial sums are reduced over
-// its input lanes with butterfly shuffles. Layout: codes [d][K][L][MP] (MP = m rounded up to
-// 1/2/4/8 bytes), P = out*spline*scale [d][K][MP] f32, Q = out*spline*y_min, CB [d][MP].
+// Small-out_dim layers (m <= 8, whole table <= ~200 KB, d <= 256): the entire layer is
+// resident in shared memory. Lane = row: each lane walks every input of its row — starting
+// at input (lane mod d) so the lanes of a warp read different inputs' tables — and keeps its
+// m outputs in registers (no cross-lane reduction). Preferred table (VT): the dequantized
+// value table V[i][k][l][MP] = f32(out*spline*(y_min + scale*q)) and CB[i][MP]; fallback for
+// larger tables: codes [i][k][l][MP] + P/Q [i][k][MP] + CB.
 struct SmallArgs {
   const uint8_t* lut;
   int32_t lut_bytes, p_off, q_off, cb_off, MP;
@@ -429,33 +423,34 @@ struct SmallArgs {
   float4 ktab[kMaxKT];
 };
 
-template <bool ASYM, bool SR, bool ZS>
-__global__ void __launch_bounds__(256) fwd_small(const __grid_constant__ SmallArgs a) {
+template <bool ASYM, bool SR, bool ZS, bool VT, int MPT>
+__global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* lut = smem;
   float4* ktab = reinterpret_cast<float4*>(smem + ((a.lut_bytes + 15) & ~15));
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = blockDim.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   for (int o = tid * 16; o < a.lut_bytes; o += blockDim.x * 16)
     *reinterpret_cast<uint4*>(lut + o) = __ldg(reinterpret_cast<const uint4*>(a.lut + o));
   for (int k = tid; k < a.cc.K; k += blockDim.x) ktab[k] = a.ktab[k];
   __syncthreads();
-  int DP = 1;
-  while (DP < a.d && DP < 32) DP <<= 1;
-  const int RPW = 32 / DP, li = lane & (DP - 1), rsub = lane / DP;
   const float lo = a.cc.lo;
-  const int K = a.cc.K, L = a.cc.L, MP = a.MP, m = a.m;
-  const int64_t x_rs = a.x_blk > 0 ? a.x_blk : a.d;
+  const int K = a.cc.K, L = a.cc.L, d = a.d, MP = VT ? MPT : a.MP;
+  const int64_t x_rs = a.x_blk > 0 ? a.x_blk : d;
+  const int i0 = lane % d;
+  const float* V = reinterpret_cast<const float*>(lut);
+  const float* CBt = reinterpret_cast<const float*>(lut + a.cb_off);
   uint32_t oob_inputs = 0, oob_rows = 0;
   bool nonfinite = false;
-  const int64_t step = (int64_t)gridDim.x * W * RPW;
-  for (int64_t rbase = ((int64_t)blockIdx.x * W + warp) * RPW; rbase < a.rows; rbase += step) {
-    const int64_t row = rbase + rsub;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t rb = (int64_t)blockIdx.x * blockDim.x; rb < a.rows; rb += stride) {
+    const int64_t row = rb + tid;
     const bool vrow = row < a.rows;
-    float part[8];
+    float y[8];
 #pragma unroll
-    for (int j = 0; j < 8; j++) part[j] = 0.0f;
+    for (int j = 0; j < 8; j++) y[j] = 0.0f;
     bool any_oob = false;
-    for (int i = li; i < a.d; i += DP) {
+    int i = i0;
+    for (int t = 0; t < d; t++, i = (i + 1 == d) ? 0 : i + 1) {
       float x = lo;
       if (vrow) {
         int64_t off;
@@ -468,50 +463,51 @@ __global__ void __launch_bounds__(256) fwd_small(const __grid_constant__ SmallAr
         x = __ldg(a.X + off);
       }
       const lkg::Coord co = lkg::lut_coords(a.cc, ktab, x);
-      const bool in = co.in;
-      const int k = co.k, l0 = co.l0;
-      const float xp = co.xp, w1 = co.w1;
       nonfinite |= !(fabsf(x) <= 3.402823466e38f);
-      oob_inputs += (uint32_t)!in;
-      any_oob |= !in;
-      const int l1 = min(l0 + 1, L - 1);
-      const float w0 = 1.0f - w1;
-      const uint8_t* c0 = lut + ((i * K + k) * L + l0) * MP;
-      const uint8_t* c1 = lut + ((i * K + k) * L + l1) * MP;
-      const float* P = reinterpret_cast<const float*>(lut + a.p_off) + (i * K + k) * MP;
-      const float* Q = reinterpret_cast<const float*>(lut + a.q_off) + (i * K + k) * MP;
-      const float* CB = reinterpret_cast<const float*>(lut + a.cb_off) + i * MP;
-      const bool tab = !(ZS && !in);
+      oob_inputs += (uint32_t)!co.in;
+      any_oob |= !co.in;
+      const bool tab = !(ZS && !co.in);
       float bx = 0.0f;
       if (SR) {
-        const float xb = ZS ? x : xp;
+        const float xb = ZS ? x : co.xp;  // clip_x clips the base branch too (runtime.cpp:189)
         bx = __fdividef(xb, 1.0f + __expf(-xb));
       }
+      const int cell = i * K + co.k, l1 = min(co.l0 + 1, L - 1);
+      const float w1 = co.w1, w0 = 1.0f - w1;
+      const float* CB = CBt + i * MP;
+      if (VT) {
+        const float* V0 = V + (cell * L + co.l0) * MPT;
+        const float* V1 = V + (cell * L + l1) * MPT;
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        if (j < m) {
-          const float q0 = ASYM ? (float)c0[j] : (float)(int8_t)c0[j];
-          const float q1 = ASYM ? (float)c1[j] : (float)(int8_t)c1[j];
-          float v = 0.0f;
-          if (tab) {
-            v = P[j] * fmaf(w1, q1, w0 * q0);
-            if (ASYM) v += Q[j];
+        for (int j = 0; j < MPT; j++) {
+          const float v = tab ? fmaf(w1, V1[j], w0 * V0[j]) : 0.0f;
+          y[j] += SR ? fmaf(CB[j], bx, v) : v;
+        }
+      } else {
+        const uint8_t* c0 = lut + (cell * L + co.l0) * MP;
+        const uint8_t* c1 = lut + (cell * L + l1) * MP;
+        const float* P = reinterpret_cast<const float*>(lut + a.p_off) + cell * MP;
+        const float* Q = reinterpret_cast<const float*>(lut + a.q_off) + cell * MP;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          if (j < MP) {
+            const float q0 = ASYM ? (float)c0[j] : (float)(int8_t)c0[j];
+            const float q1 = ASYM ? (float)c1[j] : (float)(int8_t)c1[j];
+            float v = 0.0f;
+            if (tab) {
+              v = P[j] * fmaf(w1, q1, w0 * q0);
+              if (ASYM) v += Q[j];
+            }
+            y[j] += SR ? fmaf(CB[j], bx, v) : v;
           }
-          part[j] += SR ? fmaf(CB[j], bx, v) : v;
         }
       }
     }
-    // reduce over the DP input lanes of each row
-#pragma unroll
-    for (int j = 0; j < 8; j++)
-      if (j < m)
-        for (int o = 1; o < DP; o <<= 1) part[j] += __shfl_xor_sync(0xffffffffu, part[j], o);
-    for (int o = 1; o < DP; o <<= 1) any_oob |= __shfl_xor_sync(0xffffffffu, (int)any_oob, o) != 0;
-    if (vrow && li == 0) {
-      float* yr = a.Y + row * m;
+    if (vrow) {
+      float* yr = a.Y + row * a.m;
 #pragma unroll
       for (int j = 0; j < 8; j++)
-        if (j < m) yr[j] = part[j];
+        if (j < a.m) yr[j] = y[j];
       oob_rows += any_oob;
     }
   }
@@ -525,6 +521,29 @@ __global__ void __launch_bounds__(256) fwd_small(const __grid_constant__ SmallAr
     if (oi) atomicAdd(a.counters + 1, oi);
   }
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicExch(a.counters + 2, 1ull);
+}
+
+// Dequantized value table for small layers: V[i][k][l][j] = (f32)(cs * (y_min + scale * q)),
+// cs = out*spline (1 for phi), evaluated in f64 like fetch_quant (runtime.cpp:124-128, 202-205).
+__global__ void build_small_vt_kernel(const uint8_t* q, const float* scale, const float* ymin, const float* gains,
+                                      float* V, int32_t d, int32_t m, int32_t K, int32_t L, int32_t MP,
+                                      int32_t cb_off, int sr, int sym) {
+  const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t E = (int64_t)d * m;
+  if (cell >= E * K) return;
+  const int64_t e = cell / K;
+  const int k = (int)(cell - e * K);
+  const int i = (int)(e / m), j = (int)(e - (int64_t)i * m);
+  const double cs = sr ? (double)gains[2 * E + e] * (double)gains[E + e] : 1.0;
+  const double ym = ymin[cell], sc = scale[cell];
+  for (int l = 0; l < L; l++) {
+    const uint8_t b = q[cell * L + l];
+    const double qv = sym ? (double)(int8_t)b : (double)b;
+    V[((int64_t)(i * K + k) * L + l) * MP + j] = (float)(cs * (ym + sc * qv));
+  }
+  if (sr && k == 0)
+    reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(V) + cb_off)[i * MP + j] =
+        (float)((double)gains[2 * E + e] * (double)gains[e]);
 }
 
 __global__ void build_small_kernel(const uint8_t* q, const float* scale, const float* ymin, const float* gains,
@@ -610,6 +629,24 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   // small out_dim: the whole layer in shared memory (fwd_small)
   if (m <= 8 && d <= kFp32MaxD) {
     const int MP = m <= 1 ? 1 : (m <= 2 ? 2 : (m <= 4 ? 4 : 8));
+    // preferred: dequantized value table V = out*spline*(y_min + scale*q) in f32 (one rounding of
+    // the f64 product), so the table walk is two loads and two FMAs per edge
+    const int64_t vt = ((int64_t)d * K * Ls * MP * 4 + 15) / 16 * 16;
+    const int64_t vt_total = vt + ((int64_t)d * MP * 4 + 15) / 16 * 16;
+    if (vt_total + kMaxKT * 16 <= kSmallMaxBytes) {
+      gm.small = 2;
+      gm.MP = MP;
+      gm.cb_off = (int32_t)vt;
+      gm.tile_bytes = vt_total;
+      L->tiles.alloc((size_t)vt_total);
+      LKG_CUDA(cudaMemsetAsync(L->tiles.p, 0, L->tiles.bytes, ctx->stream));
+      build_small_vt_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(
+          L->q.as<uint8_t>(), L->scale.as<float>(), L->ymin.as<float>(), L->gains.as<float>(),
+          L->tiles.as<float>(), d, m, K, Ls, MP, gm.cb_off, sr, !asym);
+      LKG_CUDA(cudaGetLastError());
+      ctx->launches++;
+      return;
+    }
     int64_t off = ((int64_t)d * K * Ls * MP + 15) / 16 * 16;
     const int64_t pq = ((int64_t)d * K * MP * 4 + 15) / 16 * 16;
     gm.p_off = (int32_t)off;
@@ -692,15 +729,15 @@ static int sm_count(int dev) {
   return sms[dev] > 0 ? sms[dev] : 148;
 }
 
-template <bool ASYM, bool SR, bool ZS>
+template <bool ASYM, bool SR, bool ZS, bool VT, int MPT>
 static void launch_small_t(cudaStream_t st, const SmallArgs& a, size_t smem, int grid) {
-  auto kern = fwd_small<ASYM, SR, ZS>;
+  auto kern = fwd_small<ASYM, SR, ZS, VT, MPT>;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  kern<<<grid, 256, smem, st>>>(a);
+  kern<<<grid, 1024, smem, st>>>(a);
 }
 
 static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk,
@@ -721,22 +758,28 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
   a.m = L->col1 - L->col0;
   a.counters = ctx->counters.as<unsigned long long>() + 4 * slot;
   fill_coord_const(L, a.cc, a.ktab);
-  int DP = 1;
-  while (DP < a.d && DP < 32) DP <<= 1;
-  const int64_t groups = (rows + (32 / DP) * 8 - 1) / ((32 / DP) * 8);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(groups, 2 * sm_count(ctx->device)));
+  const int blocks_per_sm = gm.tile_bytes <= 100 * 1024 ? 2 : 1;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 1023) / 1024, blocks_per_sm * sm_count(ctx->device)));
   const size_t smem = ((gm.tile_bytes + 15) & ~15) + kMaxKT * 16;
   const bool asym = L->scheme == LKG_SCHEME_ASYMMETRIC, sr = L->value_repr == LKG_REPR_SPLINE_COMPONENT;
   const bool zs = L->oob_policy == LKG_OOB_ZERO_SPLINE;
-  switch ((asym << 2) | (sr << 1) | (int)zs) {
-    case 0: launch_small_t<false, false, false>(ctx->stream, a, smem, grid); break;
-    case 1: launch_small_t<false, false, true>(ctx->stream, a, smem, grid); break;
-    case 2: launch_small_t<false, true, false>(ctx->stream, a, smem, grid); break;
-    case 3: launch_small_t<false, true, true>(ctx->stream, a, smem, grid); break;
-    case 4: launch_small_t<true, false, false>(ctx->stream, a, smem, grid); break;
-    case 5: launch_small_t<true, false, true>(ctx->stream, a, smem, grid); break;
-    case 6: launch_small_t<true, true, false>(ctx->stream, a, smem, grid); break;
-    default: launch_small_t<true, true, true>(ctx->stream, a, smem, grid); break;
+  const int sz = (sr << 1) | (int)zs;
+  if (gm.small == 2) {  // value table: compile-time padded out_dim
+    const int mp = gm.MP == 1 ? 0 : (gm.MP == 2 ? 1 : (gm.MP == 4 ? 2 : 3));
+    switch ((mp << 2) | sz) {
+#define CASE(S) \
+  case S: launch_small_t<false, (S >> 1) & 1, S & 1, true, 1 << (S >> 2)>(ctx->stream, a, smem, grid); break;
+      CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+      CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
+#undef CASE
+    }
+  } else {
+    switch ((asym << 2) | sz) {
+#define CASE(S) \
+  case S: launch_small_t<(S >> 2) & 1, (S >> 1) & 1, S & 1, false, 8>(ctx->stream, a, smem, grid); break;
+      CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+    }
   }
   LKG_CUDA(cudaGetLastError());
   ctx->launches++;
@@ -748,7 +791,7 @@ static size_t tiled_smem(const lkg_layer* L, int W, int R) {
 
 bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
   const TileGeom &g1 = L1->geom, &g2 = L2->geom;
-  if (!g1.tile_bytes || g1.small || g1.n_jb != 1 || !g2.tile_bytes || !g2.small) return false;
+  if (!g1.tile_bytes || g1.small || g1.n_jb != 1 || !g2.tile_bytes || g2.small != 2) return false;
   if (L1->in_dim > kFp32MaxD || L2->in_dim != L1->col1 - L1->col0 || L2->col1 - L2->col0 > 8) return false;
   if (L1->scheme != L2->scheme || L1->value_repr != L2->value_repr || L1->oob_policy != L2->oob_policy) return false;
   return tiled_smem(L1, kW, kR) + kMaxKT * 16 + ((g2.tile_bytes + 15) & ~15) <= 227 * 1024;
