@@ -137,6 +137,11 @@ lkg_status lkg_layer_free(lkg_layer* layer);
 lkg_status lkg_spec_upload(lkg_ctx* ctx, const lkg_spec_desc* desc, lkg_spec** out);
 lkg_status lkg_spec_upload_columns(lkg_ctx* ctx, const lkg_spec_desc* desc, int32_t col0,
                                    int32_t col1, lkg_spec** out);
+/* A spec that already holds only output columns [col0, col0 + desc->out_dim) of a layer whose
+ * full width is full_out_dim (each rank of a column-sharded deployment materialises only its
+ * own edges). Layers compiled from it are column shards. */
+lkg_status lkg_spec_upload_shard(lkg_ctx* ctx, const lkg_spec_desc* desc, int32_t col0, int32_t full_out_dim,
+                                 lkg_spec** out);
 lkg_status lkg_spec_free(lkg_spec* spec);
 /* compile_layer (compiler.cpp:213-216): bytes, scales and y_mins bit-exact with the
  * reference. keep_float != 0 also keeps the f64 float table (compile_layer_debug_float). */
@@ -178,6 +183,11 @@ lkg_status lkg_spline_forward(lkg_ctx* ctx, const lkg_spec* spec, const float* X
  * lkg_nccl_unique_id() on rank 0, broadcast by the host (e.g. torch.distributed). */
 lkg_status lkg_nccl_unique_id(uint8_t id_out[128]);
 lkg_status lkg_ctx_init_nccl(lkg_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank);
+/* One layer forward whose input X is in the rank-major all-gather layout of column shards of
+ * width x_blk (element (r, i) at X[(i / x_blk) * rows * x_blk + r * x_blk + i % x_blk]), i.e.
+ * ncclAllGather output consumed in place; x_blk == 0 means row-major. Device pointers. */
+lkg_status lkg_layer_forward_blocked(lkg_ctx* ctx, const lkg_layer* layer, const float* X, int64_t rows,
+                                     int32_t x_blk, float* Y, lkg_oob_stats* stats);
 /* Column-sharded chain: every rank holds the column shard [col0, col1) of every layer
  * (equal shards, rank-ordered). X [rows, in_dim] replicated; between layers the local
  * outputs are all-gathered over NCCL (rank-major blocks consumed in place); Y receives the

@@ -69,6 +69,7 @@ SIGNATURES = {
     "lkg_layer_free": (C.c_int, [C.c_void_p]),
     "lkg_spec_upload": (C.c_int, [C.c_void_p, _P(SpecDesc), _P(C.c_void_p)]),
     "lkg_spec_upload_columns": (C.c_int, [C.c_void_p, _P(SpecDesc), C.c_int32, C.c_int32, _P(C.c_void_p)]),
+    "lkg_spec_upload_shard": (C.c_int, [C.c_void_p, _P(SpecDesc), C.c_int32, C.c_int32, _P(C.c_void_p)]),
     "lkg_spec_free": (C.c_int, [C.c_void_p]),
     "lkg_compile_layer": (C.c_int, [C.c_void_p, C.c_void_p, _P(QuantCfg), _P(OobCfg), C.c_int32, _P(C.c_void_p)]),
     "lkg_layer_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, _P(OobStatsC)]),
@@ -76,6 +77,8 @@ SIGNATURES = {
                                     _P(OobStatsC)]),
     "lkg_model_forward_host": (C.c_int, [C.c_void_p, _P(C.c_void_p), C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
                                          _P(OobStatsC)]),
+    "lkg_layer_forward_blocked": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
+                                            _P(OobStatsC)]),
     "lkg_layer_coords": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                    C.c_void_p]),
     "lkg_ctx_collect": (C.c_int, [C.c_void_p, _P(OobStatsC), C.c_int32]),

@@ -389,6 +389,19 @@ lkg_status lkg_spec_upload_columns(lkg_ctx* ctx, const lkg_spec_desc* desc, int3
                                    lkg_spec** out) {
   return spec_upload_impl(ctx, desc, col0, col1, out);
 }
+lkg_status lkg_spec_upload_shard(lkg_ctx* ctx, const lkg_spec_desc* desc, int32_t col0, int32_t full_out_dim,
+                                 lkg_spec** out) {
+  const lkg_status st = spec_upload_impl(ctx, desc, 0, desc ? desc->out_dim : 0, out);
+  if (st != LKG_OK) return st;
+  return guarded([&] {
+    if (col0 < 0 || full_out_dim < col0 + desc->out_dim) {
+      lkg_spec_free(*out);
+      *out = nullptr;
+      fail(LKG_ERR_DIMENSION, "shard columns outside the full layer width");
+    }
+    (*out)->full_out_dim = full_out_dim;
+  });
+}
 lkg_status lkg_spec_free(lkg_spec* S) {
   return guarded([&] {
     if (!S) return;
@@ -609,6 +622,26 @@ lkg_status lkg_model_forward_host(lkg_ctx* ctx, const lkg_layer* const* chain, i
   });
 }
 
+lkg_status lkg_layer_forward_blocked(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk,
+                                     float* Y, lkg_oob_stats* stats) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(L, "layer");
+    if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
+    if (x_blk < 0 || (x_blk > 0 && L->in_dim % x_blk != 0))
+      fail(LKG_ERR_DIMENSION, "block width must divide in_dim");
+    if (rows > 0) {
+      need(X, "X");
+      need(Y, "Y");
+    }
+    DeviceGuard g(ctx->device);
+    lkg::launch_forward(ctx, L, X, rows, x_blk, Y, 0, true);
+    ctx->rows_seen[0] += (uint64_t)rows;
+    ctx->in_dim_seen[0] = L->in_dim;
+    if (stats) collect_impl(ctx, stats, 1);
+  });
+}
+
 lkg_status lkg_layer_coords(lkg_ctx* ctx, const lkg_layer* L, const float* x, int64_t n, int32_t* in_range,
                             int32_t* k, int32_t* l0) {
   return guarded([&] {
@@ -706,7 +739,7 @@ lkg_status lkg_model_forward_sharded(lkg_ctx* ctx, const lkg_layer* const* chain
       ctx->in_dim_seen[l] = chain[l]->in_dim;
       if (!last) {
         const size_t cnt = (size_t)rows * chain[l]->out_dim;
-        if (G > 1) {
+        if (ctx->nccl) {
           const ncclResult_t r = ncclAllGather(dst, ctx->gather.p, cnt, ncclFloat, static_cast<ncclComm_t>(ctx->nccl),
                                                ctx->stream);
           if (r != ncclSuccess) fail(LKG_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));

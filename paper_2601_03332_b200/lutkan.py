@@ -272,6 +272,10 @@ class KanLayerSpec:
     spline_scale: np.ndarray
     out_scale: np.ndarray
     base_kind: str = "silu"
+    # column-shard placement: this spec holds columns [col0, col0 + out_dim) of a layer whose
+    # full width is full_out_dim (0 = not a shard)
+    col0: int = 0
+    full_out_dim: int = 0
     _dev: dict = field(default_factory=dict, repr=False)
 
     def edge_count(self) -> int:
@@ -291,6 +295,8 @@ class KanLayerSpec:
             h = C.c_void_p()
             if col1 > col0:
                 check(lib().lkg_spec_upload_columns(engine.handle, C.byref(d), col0, col1, C.byref(h)))
+            elif self.full_out_dim:
+                check(lib().lkg_spec_upload_shard(engine.handle, C.byref(d), self.col0, self.full_out_dim, C.byref(h)))
             else:
                 check(lib().lkg_spec_upload(engine.handle, C.byref(d), C.byref(h)))
             self._dev[key] = DeviceSpec(h, self.in_dim, (col1 - col0) if col1 > col0 else self.out_dim)
@@ -604,7 +610,10 @@ def recipe_layer(cfg: int, layer: int, col0: int = 0, col1: int = 0) -> KanLayer
     bp, co = np.zeros(G + 1), np.zeros(E * R)
     bs, ss, os_ = np.zeros(E), np.zeros(E), np.zeros(E)
     check(lib().lkg_recipe_layer(cfg, layer, col0, col1, *[a.ctypes.data_as(_capi.f64p) for a in (bp, co, bs, ss, os_)]))
-    return KanLayerSpec(d, mc, KnotGrid(bp, 3), co.reshape(E, R), bs, ss, os_)
+    spec = KanLayerSpec(d, mc, KnotGrid(bp, 3), co.reshape(E, R), bs, ss, os_)
+    if col1 > col0:
+        spec.col0, spec.full_out_dim = col0, m
+    return spec
 
 
 def recipe_inputs(cfg: int, row0: int, rows: int, out: np.ndarray | None = None) -> np.ndarray:
