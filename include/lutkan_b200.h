@@ -177,6 +177,9 @@ lkg_status lkg_ctx_collect(lkg_ctx* ctx, lkg_oob_stats* stats, int32_t n_layers)
 /* layer_forward_batch(spec, X, Tier::Optimized) (spline.cpp:145-187); device pointers. */
 lkg_status lkg_spline_forward(lkg_ctx* ctx, const lkg_spec* spec, const float* X, int64_t rows,
                               float* Y);
+/* Same with HOST buffers (H2D of X, kernel, D2H of Y; synchronous). */
+lkg_status lkg_spline_forward_host(lkg_ctx* ctx, const lkg_spec* spec, const float* X_host, int64_t rows,
+                                   float* Y_host);
 
 /* ------------------------------------------------ multi-GPU (column shards) */
 /* NCCL communicator for output-column sharding. id: 128 bytes from

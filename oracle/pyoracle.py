@@ -124,6 +124,9 @@ def build(ref: bool = True) -> None:
     targets = ["port"]
     if ref and os.path.isdir("/root/reference/proj/core/src"):
         targets.append("ref")
+        lib = os.path.join(os.path.dirname(HERE), "paper_2601_03332_b200", "liblutkan_b200.so")
+        if os.path.exists(lib):
+            targets.append("shim")  # C++ drop-in shim test against the reference library
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 

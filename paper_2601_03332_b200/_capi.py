@@ -83,6 +83,7 @@ SIGNATURES = {
                                    C.c_void_p]),
     "lkg_ctx_collect": (C.c_int, [C.c_void_p, _P(OobStatsC), C.c_int32]),
     "lkg_spline_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "lkg_spline_forward_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "lkg_nccl_unique_id": (C.c_int, [_P(C.c_uint8)]),
     "lkg_ctx_init_nccl": (C.c_int, [C.c_void_p, _P(C.c_uint8), C.c_int32, C.c_int32]),
     "lkg_model_forward_sharded": (C.c_int, [C.c_void_p, _P(C.c_void_p), C.c_int32, C.c_void_p, C.c_int64,

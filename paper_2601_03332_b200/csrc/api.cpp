@@ -676,6 +676,26 @@ lkg_status lkg_spline_forward(lkg_ctx* ctx, const lkg_spec* S, const float* X, i
   });
 }
 
+lkg_status lkg_spline_forward_host(lkg_ctx* ctx, const lkg_spec* S, const float* Xh, int64_t rows, float* Yh) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(S, "spec");
+    if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
+    if (rows == 0) return;
+    need(Xh, "X");
+    need(Yh, "Y");
+    DeviceGuard g(ctx->device);
+    const size_t xb = sizeof(float) * rows * S->in_dim, yb = sizeof(float) * rows * (S->col1 - S->col0);
+    ensure(ctx->hostio, xb + yb + 256);
+    float* dX = ctx->hostio.as<float>();
+    float* dY = reinterpret_cast<float*>(ctx->hostio.as<char>() + ((xb + 255) / 256) * 256);
+    LKG_CUDA(cudaMemcpyAsync(dX, Xh, xb, cudaMemcpyHostToDevice, ctx->stream));
+    lkg::launch_spline(ctx, S, dX, rows, dY, nullptr);
+    LKG_CUDA(cudaMemcpyAsync(Yh, dY, yb, cudaMemcpyDeviceToHost, ctx->stream));
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 // ---------------------------------------------------------------- multi-GPU
 lkg_status lkg_nccl_unique_id(uint8_t id_out[128]) {
   return guarded([&] {

@@ -577,17 +577,14 @@ def layer_forward_batch(layer: KanLayerSpec, X, tier: Tier = Tier.Optimized, eng
         check(lib().lkg_spline_forward(eng.handle, spec.handle, C.c_void_p(X.data_ptr()), X.shape[0],
                                        C.c_void_p(Y.data_ptr())))
         return Y
-    import torch  # device staging for host batches
     X = np.asarray(X)
     if X.ndim != 2 or X.shape[1] != layer.in_dim:
         raise DimensionError("batch column count does not match in_dim")
-    Xd = torch.from_numpy(np.ascontiguousarray(X, np.float32)).to(f"cuda:{eng.device}")
-    Yd = torch.empty((X.shape[0], layer.out_dim), device=Xd.device, dtype=torch.float32)
-    torch.cuda.synchronize(Xd.device)
-    check(lib().lkg_spline_forward(eng.handle, spec.handle, C.c_void_p(Xd.data_ptr()), X.shape[0],
-                                   C.c_void_p(Yd.data_ptr())))
-    eng.synchronize()
-    return Yd.cpu().numpy()
+    X = np.ascontiguousarray(X, np.float32)
+    Y = np.zeros((X.shape[0], layer.out_dim), np.float32)
+    check(lib().lkg_spline_forward_host(eng.handle, spec.handle, X.ctypes.data_as(C.c_void_p), X.shape[0],
+                                        Y.ctypes.data_as(C.c_void_p)))
+    return Y
 
 
 # ------------------------------------------------------------------ recipes

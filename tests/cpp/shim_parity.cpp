@@ -1,0 +1,121 @@
+// shim_parity.cpp — the C++ drop-in shim (include/lutkan_b200.hpp) exercised against the
+// UNMODIFIED reference library (oracle/_ref/liblutkan_ref.a, built in place from the reference
+// sources), in the style of the reference's own tests (tests/test_runtime.cpp,
+// tests/test_compiler.cpp). Built by oracle/Makefile (target `shim`) where /root/reference
+// exists; run on the GPU box by tests/test_gpu_shim.py. Prints one line per check and exits
+// non-zero on the first failure.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "lutkan/compiler.hpp"
+#include "lutkan/model_gen.hpp"
+#include "lutkan/runtime.hpp"
+#include "lutkan/spline.hpp"
+#include "lutkan_b200.hpp"
+
+using namespace lutkan;
+
+static int fails = 0;
+#define CHECK(cond, what)                                    \
+  do {                                                       \
+    if (!(cond)) {                                           \
+      std::printf("[FAIL] %s (%s:%d)\n", what, __FILE__, __LINE__); \
+      fails++;                                               \
+    } else {                                                 \
+      std::printf("[PASS] %s\n", what);                      \
+    }                                                        \
+  } while (0)
+
+static double max_err(const Matrix& a, const Matrix& b) {
+  double m = 0;
+  for (size_t i = 0; i < a.data.size(); i++) {
+    const double d = std::fabs(a.data[i] - b.data[i]);
+    const double tol = std::fabs(b.data[i]) > 1.0 ? 1e-5 * std::fabs(b.data[i]) : 1e-5;
+    m = std::fmax(m, d / tol * 1e-5);
+  }
+  return m;
+}
+
+int main() {
+  // compile parity: bytes identical to lutkan::compile_layer (test_compiler.cpp:269-281 style)
+  for (Scheme sch : {Scheme::Symmetric, Scheme::Asymmetric}) {
+    QuantConfig cfg;
+    cfg.samples_per_segment = 32;
+    cfg.scheme = sch;
+    cfg.dtype = sch == Scheme::Symmetric ? Dtype::Int8 : Dtype::Uint8;
+    const KanLayerSpec layer = gen_layer(11, 24, 12, 8, 3);
+    const OobConfig oob{BoundaryMode::HalfOpen, OobPolicy::ZeroSpline};
+    const LutLayerArtifact ref = lutkan::compile_layer(layer, cfg, oob);
+    const LutLayerArtifact gpu = lutkan_b200::compile_layer(layer, cfg, oob);
+    CHECK(ref.q_table == gpu.q_table && ref.scale == gpu.scale && ref.y_min == gpu.y_min &&
+              ref.knots == gpu.knots && ref.edge_out_scale == gpu.edge_out_scale,
+          sch == Scheme::Symmetric ? "compile_layer bytes (int8 symmetric)" : "compile_layer bytes (uint8 asymmetric)");
+    // forward parity on seeded inputs that spill past the domain (test_runtime.cpp:328-344 style)
+    const Matrix X = gen_inputs(53, 2000, 24, -1.3, 1.3, false);
+    Matrix Xf = X;
+    for (double& v : Xf.data) v = static_cast<double>(static_cast<float>(v));
+    const auto [yr, sr] = lutkan::lut_layer_forward_batch(ref, Xf, Tier::Optimized);
+    const auto [yg, sg] = lutkan_b200::lut_layer_forward_batch(gpu, Xf, Tier::Optimized);
+    CHECK(max_err(yg, yr) <= 1e-5, "lut_layer_forward_batch within 1e-5");
+    CHECK(sr.n_oob_inputs == sg.n_oob_inputs && sr.n_oob_samples == sg.n_oob_samples && sr.n_samples == sg.n_samples &&
+              sr.n_inputs == sg.n_inputs,
+          "OobStats identical");
+    const Matrix ys_ref = lutkan::layer_forward_batch(layer, Xf, Tier::Optimized);
+    const Matrix ys_gpu = lutkan_b200::layer_forward_batch(layer, Xf, Tier::Optimized);
+    CHECK(max_err(ys_gpu, ys_ref) <= 1e-5, "layer_forward_batch (spline) within 1e-5");
+  }
+  // chains and their error behaviour (test_runtime.cpp:256-296 style)
+  {
+    QuantConfig cfg;
+    const std::vector<KanLayerSpec> layers = {gen_layer(7, 10, 8, 8, 3), gen_layer(8, 8, 3, 8, 3)};
+    const OobConfig oob{};
+    const auto ref = lutkan::compile_model(layers, cfg, oob);
+    const auto gpu = lutkan_b200::compile_model(layers, cfg, oob);
+    const Matrix X = gen_inputs(9, 500, 10, -1.0, 1.0, true);
+    Matrix Xf = X;
+    for (double& v : Xf.data) v = static_cast<double>(static_cast<float>(v));
+    const auto cr = lutkan::lut_model_forward_batch(ref, Xf, Tier::Optimized);
+    const auto cg = lutkan_b200::lut_model_forward_batch(gpu, Xf, Tier::Optimized);
+    int agree = 0;
+    for (size_t r = 0; r < X.rows; r++) {
+      int a = 0, b = 0;
+      for (int j = 1; j < 3; j++) {
+        if (cr.Y.at(r, j) > cr.Y.at(r, a)) a = j;
+        if (cg.Y.at(r, j) > cg.Y.at(r, b)) b = j;
+      }
+      agree += a == b;
+    }
+    CHECK(agree == static_cast<int>(X.rows), "lut_model_forward_batch argmax classes identical");
+    CHECK(cr.per_layer.size() == cg.per_layer.size() && cr.per_layer[0].n_oob_inputs == cg.per_layer[0].n_oob_inputs,
+          "chain per-layer OobStats");
+    bool threw = false;
+    try {
+      lutkan_b200::lut_model_forward_batch({}, Xf);
+    } catch (const ConfigError&) {
+      threw = true;
+    }
+    CHECK(threw, "empty chain -> ConfigError");
+    threw = false;
+    Matrix bad(1, 1);
+    bad.at(0, 0) = NAN;
+    try {
+      lutkan_b200::lut_layer_forward_batch(gpu[0], Matrix(1, 3));
+    } catch (const DimensionError&) {
+      threw = true;
+    }
+    CHECK(threw, "column mismatch -> DimensionError");
+    threw = false;
+    Matrix nf(2, 10);
+    nf.at(1, 4) = INFINITY;
+    try {
+      lutkan_b200::lut_layer_forward_batch(gpu[0], nf);
+    } catch (const NonFiniteError&) {
+      threw = true;
+    }
+    CHECK(threw, "non-finite input -> NonFiniteError");
+  }
+  std::printf("%s: %d failure(s)\n", fails ? "FAILED" : "OK", fails);
+  return fails ? 1 : 0;
+}
