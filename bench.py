@@ -48,23 +48,35 @@ def _env_int(k, d):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled every ~2 ms during the timed region (NVML, the
+    library behind nvidia-smi's clocks/clocks_event_reasons fields)."""
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
     def __init__(self, device: int):
         self.device, self.samples, self._stop = device, [], threading.Event()
+        self.max_mhz = None
 
     def _run(self):
-        while not self._stop.is_set():
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                     nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                self._stop.wait(0.002)
+        except Exception as ex:  # NVML unavailable: fall back to one nvidia-smi reading
+            self.error = repr(ex)
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
-                self.samples.append([s.strip() for s in out.strip().split(",")])
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=10).stdout.split(",")
+                self.samples.append((float(out[0]), 0))
+                self.max_mhz = float(out[1])
             except Exception:
                 pass
-            self._stop.wait(0.1)
 
     def __enter__(self):
         self.t = threading.Thread(target=self._run, daemon=True)
@@ -76,12 +88,10 @@ class ClockSampler:
         self.t.join(timeout=10)
 
     def summary(self):
-        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples if len(s) >= 7 for i in range(4) if s[3 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({n for _, r in self.samples for n, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples)}
 
 
 def run_reference(args, wl):
@@ -96,7 +106,8 @@ def run_reference(args, wl):
     chain = [o.compile_layer(o.recipe_layer(cfg, l), L, scheme, 1, 0, bm, op) for l in range(len(dims) - 1)]
     ee_row = sum(dims[l] * dims[l + 1] for l in range(len(dims) - 1))
     nthreads = os.cpu_count() or 1
-    sample_rows = sample_rows_for(ee_row, nthreads, rows)
+    # bounded per-step sample so the whole --steps/--warmup run stays within ~2 minutes
+    sample_rows = sample_rows_for(ee_row, nthreads, rows, seconds=min(3.0, 100.0 / (args.steps + args.warmup)))
     X = o.recipe_inputs(cfg, 0, sample_rows).astype(np.float64)
     for _ in range(args.warmup):
         o.lut_model_forward(chain, X[: max(1, sample_rows // 10)], 1, nthreads)
@@ -118,6 +129,16 @@ def run_reference(args, wl):
                                        f"Tier::Optimized, rows sharded over {nthreads} threads)"},
             "e2e": {"value": value, "unit": "edge-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def ncu_traffic(workload, layer):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
+    committed `ncu --set full` capture summary (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(f"{workload}/layer{layer}")
+    except (OSError, ValueError):
+        return None
 
 
 def o_dims(cfg):
@@ -151,8 +172,8 @@ def cpu_baseline(wl):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -243,7 +264,7 @@ def main():
     alg_bytes = rows * dims[big] * dims[big + 1] * BYTES_PER_EE[scheme]
     achieved = alg_bytes / (ms_l1 * 1e-3) / 1e9
     roofline = {"bound": "smem", "achieved": achieved, "peak": SMEM_PEAK_GBS, "unit": "GB/s",
-                "frac": achieved / SMEM_PEAK_GBS, "traffic": None,
+                "frac": achieved / SMEM_PEAK_GBS, "traffic": ncu_traffic(args.workload, big),
                 "kernel": f"layer {big} forward ({dims[big]}->{dims[big + 1]}), {ms_l1:.4f} ms/launch",
                 "peak_source": "measured LDS.128 conflict-free throughput (tools/microbench/opbench.cu, 148 SMs); "
                                "algorithmic bytes = 2 code B + 4 B scale (+4 B y_min asym) per edge-eval",

@@ -198,6 +198,14 @@ lkg_status lkg_ctx_destroy(lkg_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl));
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->copy_stream) {
+      cudaStreamSynchronize(ctx->copy_stream);
+      cudaStreamDestroy(ctx->copy_stream);
+      for (int b = 0; b < 2; b++) {
+        cudaEventDestroy(ctx->ev_copied[b]);
+        cudaEventDestroy(ctx->ev_done[b]);
+      }
+    }
     delete ctx;
   });
 }
@@ -606,16 +614,43 @@ lkg_status lkg_model_forward_host(lkg_ctx* ctx, const lkg_layer* const* chain, i
     check_chain(chain, n);
     if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
     DeviceGuard g(ctx->device);
-    const size_t xb = sizeof(float) * rows * chain[0]->in_dim, yb = sizeof(float) * rows * chain[n - 1]->out_dim;
-    ensure(ctx->hostio, xb + yb + 256);
-    float* dX = ctx->hostio.as<float>();
-    float* dY = reinterpret_cast<float*>(ctx->hostio.as<char>() + ((xb + 255) / 256) * 256);
+    const int64_t d = chain[0]->in_dim, mo = chain[n - 1]->out_dim;
+    // Row chunks of ~32 MB of X: the H2D copy of chunk c+1 (copy stream) overlaps the chain on
+    // chunk c (context stream); two device input buffers, event-ordered.
+    const int64_t ch = std::max<int64_t>(65536, (32ll << 20) / (4 * d));
+    const int64_t nch = rows > ch ? (rows + ch - 1) / ch : 1, cr = nch > 1 ? ch : rows;
+    const size_t xb = sizeof(float) * cr * d, yb = sizeof(float) * rows * mo;
+    const size_t xstride = ((xb + 255) / 256) * 256;
+    ensure(ctx->hostio, (nch > 1 ? 2 : 1) * xstride + yb + 256);
+    float* dXb[2] = {ctx->hostio.as<float>(), reinterpret_cast<float*>(ctx->hostio.as<char>() + xstride)};
+    float* dY = reinterpret_cast<float*>(ctx->hostio.as<char>() + (nch > 1 ? 2 : 1) * xstride);
     if (rows > 0) {
       need(Xh, "X");
       need(Yh, "Y");
-      LKG_CUDA(cudaMemcpyAsync(dX, Xh, xb, cudaMemcpyHostToDevice, ctx->stream));
     }
-    run_chain(ctx, chain, n, dX, rows, dY);
+    if (nch == 1) {
+      if (rows > 0) LKG_CUDA(cudaMemcpyAsync(dXb[0], Xh, xb, cudaMemcpyHostToDevice, ctx->stream));
+      run_chain(ctx, chain, n, dXb[0], rows, dY);
+    } else {
+      if (!ctx->copy_stream) {
+        LKG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; b++) {
+          LKG_CUDA(cudaEventCreateWithFlags(&ctx->ev_copied[b], cudaEventDisableTiming));
+          LKG_CUDA(cudaEventCreateWithFlags(&ctx->ev_done[b], cudaEventDisableTiming));
+        }
+      }
+      for (int64_t c = 0; c < nch; c++) {
+        const int b = (int)(c & 1);
+        const int64_t r0 = c * ch, nr = std::min(ch, rows - r0);
+        if (c >= 2) LKG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_done[b], 0));
+        LKG_CUDA(cudaMemcpyAsync(dXb[b], Xh + r0 * d, sizeof(float) * nr * d, cudaMemcpyHostToDevice,
+                                 ctx->copy_stream));
+        LKG_CUDA(cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
+        LKG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
+        run_chain(ctx, chain, n, dXb[b], nr, dY + r0 * mo);
+        LKG_CUDA(cudaEventRecord(ctx->ev_done[b], ctx->stream));
+      }
+    }
     if (rows > 0) LKG_CUDA(cudaMemcpyAsync(Yh, dY, yb, cudaMemcpyDeviceToHost, ctx->stream));
     if (stats) collect_impl(ctx, stats, n);
     else LKG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -106,6 +106,8 @@ struct lkg_ctx {
   lkg::DBuf scratch[2];  // hidden activations ping-pong
   lkg::DBuf gather;      // sharded chain: all-gathered hidden activations
   lkg::DBuf hostio;      // device staging for lkg_model_forward_host
+  cudaStream_t copy_stream = nullptr;  // H2D of the next chunk overlaps the chain on `stream`
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
   void* nccl = nullptr;  // ncclComm_t
   int32_t nranks = 1, rank = 0;
 };
