@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liblutkan_b200.so")
+LIB_PATH = os.environ.get("LKG_LIB") or os.path.join(PKG, "liblutkan_b200.so")  # LKG_LIB: A/B experiments
 
 _P = C.POINTER
 f32p, f64p, u8p, i32p = _P(C.c_float), _P(C.c_double), _P(C.c_uint8), _P(C.c_int32)

@@ -33,6 +33,7 @@
 #include <cmath>
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "coords.cuh"
@@ -109,8 +110,8 @@ __device__ __forceinline__ float magic(uint32_t w, uint32_t sel) {
   return __uint_as_float(__byte_perm(w, 0x4B000000u, sel));  // 2^23 + byte
 }
 
-template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE>
-__global__ void __launch_bounds__(W * 32, 1) fwd_tiled(const __grid_constant__ TiledArgs a) {
+template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1>
+__global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int NS = 2;
   constexpr int ROWS_W = 32 * R;        // rows per warp
@@ -587,9 +588,9 @@ __global__ void build_tiles_kernel(const uint8_t* q, const float* scale, const f
     *reinterpret_cast<float*>(t + cb_off + il * PROW + jl * 4) = (float)((double)gains[2 * E + e] * (double)gains[e]);
 }
 
-template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false>
+template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1>
 void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
-  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE>;
+  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB>;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -830,6 +831,22 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   const int grid = (int)std::min<int64_t>(a.n_items, sm_count(ctx->device));
   size_t smem = tiled_smem(L, W, R);
   const int sel = (asym << 2) | (sr << 1) | (int)zs;
+  static const char* exp_cfg = getenv("LKG_TILED_CFG");  // tuning experiments (sym, spline_component, clip_x)
+  if (exp_cfg && !L2 && !f64 && sel == 2) {
+    int ew = 16, er = 2, eb = 1;
+    sscanf(exp_cfg, "%d,%d,%d", &ew, &er, &eb);
+    a.n_items = ((rows + (int64_t)ew * 32 * er - 1) / ((int64_t)ew * 32 * er)) * gm.n_jb;
+    const int g2 = (int)std::min<int64_t>(a.n_items, (int64_t)eb * sm_count(ctx->device));
+    const size_t sm2 = tiled_smem(L, ew, er);
+    if (ew == 16 && er == 1 && eb == 2) launch_tiled<1, 16, false, true, false, false, false, 2>(ctx->stream, a, sm2, g2);
+    else if (ew == 12 && er == 2) launch_tiled<2, 12, false, true, false, false, false, 1>(ctx->stream, a, sm2, g2);
+    else if (ew == 32 && er == 1) launch_tiled<1, 32, false, true, false, false, false, 1>(ctx->stream, a, sm2, g2);
+    else if (ew == 8 && er == 2 && eb == 2) launch_tiled<2, 8, false, true, false, false, false, 2>(ctx->stream, a, sm2, g2);
+    else throw Error{LKG_ERR_INVALID_ARG, "unknown LKG_TILED_CFG"};
+    LKG_CUDA(cudaGetLastError());
+    ctx->launches++;
+    return;
+  }
   if (L2) {  // fused chain step: this layer + the small next layer in one launch
     const TileGeom& g2 = L2->geom;
     a.lut2 = L2->tiles.as<uint8_t>();
