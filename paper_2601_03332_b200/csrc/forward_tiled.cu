@@ -46,7 +46,7 @@ constexpr int G = 8;                // inputs per line
 constexpr int JB = 16;              // outputs per line / j-block
 constexpr int LINE = G * JB;        // 128 bytes
 constexpr int PROW = 80;            // bytes per P/Q/CB row (16 floats + 16 B pad, conflict-free)
-constexpr int kFlushBlocks = 8;     // f64 flush every 8 tiles = 64 inputs
+constexpr int kFlushBlocks = 1;     // f64 flush after every tile (8 inputs): partial sums stay short
 constexpr int kFp32MaxD = 256;      // fp32 accumulation bound
 
 struct TiledArgs {
@@ -61,7 +61,7 @@ struct TiledArgs {
   int32_t m;
   unsigned long long* counters;
   lkg::CoordConst cc;        // coordinate constants (coords.cuh)
-  int64_t n_items;
+  int64_t n_items, n_rt;
   float4 ktab[kMaxKT];  // {T_k, T_k+1, (L-1)/(T_k+1 - T_k), 0}
   // fused next layer (FUSE): a small-out_dim layer evaluated in the epilogue from the 16 hidden
   // activations each lane holds (the whole-layer "small" layout, resident in shared memory)
@@ -110,7 +110,7 @@ __device__ __forceinline__ float magic(uint32_t w, uint32_t sel) {
   return __uint_as_float(__byte_perm(w, 0x4B000000u, sel));  // 2^23 + byte
 }
 
-template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1>
+template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1, bool GC = false>
 __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr int NS = 2;
@@ -119,9 +119,13 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   constexpr int NX = 4 * R;             // float2 x loads per lane per tile
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t tb = a.tile_bytes;
-  uint8_t* stage = smem;                                                  // NS * tile_bytes
-  float* xs = reinterpret_cast<float*>(smem + NS * tb) + warp * G * XS;  // per-warp x tile
-  float4* ktab = reinterpret_cast<float4*>(smem + NS * tb + W * G * XS * 4);
+  // GC (codes in global): tiles whose code block exceeds shared memory (K*L large, e.g. configs[4])
+  // stage only P/Q/CB; the two code lines per (row, input) are read through the read-only path
+  // from L2, and items are ordered row-tile fastest so concurrent CTAs share each tile in L2.
+  const int64_t so = GC ? a.p_off : 0, sb = tb - so;
+  uint8_t* stage = smem;                                                  // NS * sb
+  float* xs = reinterpret_cast<float*>(smem + NS * sb) + warp * G * XS;  // per-warp x tile
+  float4* ktab = reinterpret_cast<float4*>(smem + NS * sb + W * G * XS * 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + kMaxKT);
   float4* ktab2 = reinterpret_cast<float4*>(full + 4);
   uint8_t* lut2 = reinterpret_cast<uint8_t*>(ktab2 + kMaxKT);
@@ -142,12 +146,12 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   const int64_t n_stages = n_local * a.n_ih;
   auto issue = [&](int64_t g) {
     const int64_t item = blockIdx.x + (g / a.n_ih) * gridDim.x;
-    const int jb = (int)(item % a.n_jb), ih = (int)(g % a.n_ih);
-    const uint8_t* src = a.tiles + ((int64_t)jb * a.n_ih + ih) * tb;
-    uint8_t* dst = stage + (g % NS) * tb;
-    mbar_expect_tx(&full[g % NS], (uint32_t)tb);
-    for (int64_t off = 0; off < tb; off += 32768) {
-      const uint32_t n = (uint32_t)(tb - off < 32768 ? tb - off : 32768);
+    const int jb = GC ? (int)(item / a.n_rt) : (int)(item % a.n_jb), ih = (int)(g % a.n_ih);
+    const uint8_t* src = a.tiles + ((int64_t)jb * a.n_ih + ih) * tb + so;
+    uint8_t* dst = stage + (g % NS) * sb;
+    mbar_expect_tx(&full[g % NS], (uint32_t)sb);
+    for (int64_t off = 0; off < sb; off += 32768) {
+      const uint32_t n = (uint32_t)(sb - off < 32768 ? sb - off : 32768);
       bulk_g2s(dst + off, src + off, n, &full[g % NS]);
     }
   };
@@ -167,8 +171,8 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
 
   for (int64_t li = 0; li < n_local; li++) {
     const int64_t item = blockIdx.x + li * gridDim.x;
-    const int64_t rt = item / a.n_jb;
-    const int jb = (int)(item % a.n_jb);
+    const int64_t rt = GC ? item % a.n_rt : item / a.n_jb;
+    const int jb = GC ? (int)(item / a.n_rt) : (int)(item % a.n_jb);
     const int cnt = jb == 0;  // OOB statistics are counted once per row (j-block 0)
     const int64_t row0 = rt * (int64_t)(W * ROWS_W) + warp * ROWS_W;
     const int64_t rows_left = a.rows - row0;  // rows of this warp: [0, min(ROWS_W, rows_left))
@@ -225,12 +229,13 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       __syncwarp();
       if (ih + 1 < a.n_ih) LOAD_XBLOCK(ih + 1);
       mbar_wait(&full[g % NS], (uint32_t)((g / NS) & 1));
-      const uint8_t* T = stage + (g % NS) * tb;
+      const uint8_t* T = stage + (g % NS) * sb - so;  // T + p_off is the staged P block
+      const uint8_t* Tcodes = GC ? a.tiles + ((int64_t)jb * a.n_ih + ih) * tb : T;
 
 #pragma unroll 1
       for (int s = 0; s < G; s++) {
         const int il = (s + lane) & 7;
-        const uint8_t* Tq = T + il * JB;
+        const uint8_t* Tq = Tcodes + il * JB;
         const uint8_t* Tp = T + a.p_off + il * PROW;
         float2 cb[8];
         if (SR) {
@@ -256,8 +261,9 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           const float w0 = 1.0f - w1;
           const float cA = -fmaf(w0, M, OFF), cB = -w1 * M;
           const uint8_t* qp = Tq + (k * L + l0) * LINE;
-          const uint4 c0 = *reinterpret_cast<const uint4*>(qp);
-          const uint4 c1 = *reinterpret_cast<const uint4*>(qp + LINE);
+          const uint4 c0 = GC ? __ldg(reinterpret_cast<const uint4*>(qp)) : *reinterpret_cast<const uint4*>(qp);
+          const uint4 c1 =
+              GC ? __ldg(reinterpret_cast<const uint4*>(qp + LINE)) : *reinterpret_cast<const uint4*>(qp + LINE);
           const int prow = ((ZS && !in) ? K : k) * (G * PROW);  // zero block masks the table term
           const float4* pp = reinterpret_cast<const float4*>(Tp + prow);
           float bx = 0.0f;
@@ -588,9 +594,9 @@ __global__ void build_tiles_kernel(const uint8_t* q, const float* scale, const f
     *reinterpret_cast<float*>(t + cb_off + il * PROW + jl * 4) = (float)((double)gains[2 * E + e] * (double)gains[e]);
 }
 
-template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1>
+template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1, bool GC = false>
 void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
-  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB>;
+  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC>;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -683,7 +689,8 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   }
   off = (off + 127) / 128 * 128;
   const size_t xs_bytes = (size_t)kW * G * (32 * kR + 4) * 4;
-  if (2 * off + xs_bytes + kMaxKT * 16 + 32 > 227 * 1024) return;  // tile too large: generic kernel
+  gm.codes_global = 2 * off + xs_bytes + kMaxKT * 16 + 32 > 227 * 1024;  // codes stay in global (L2)
+  if (gm.codes_global && 2 * (off - gm.p_off) + xs_bytes + kMaxKT * 16 + 32 > 227 * 1024) return;  // generic
   gm.tile_bytes = off;
   gm.JB = JB;
   gm.IC = G;
@@ -787,12 +794,13 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
 }
 
 static size_t tiled_smem(const lkg_layer* L, int W, int R) {
-  return 2 * L->geom.tile_bytes + (size_t)W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 32;
+  const int64_t sb = L->geom.tile_bytes - (L->geom.codes_global ? L->geom.p_off : 0);
+  return 2 * sb + (size_t)W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 32;
 }
 
 bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
   const TileGeom &g1 = L1->geom, &g2 = L2->geom;
-  if (!g1.tile_bytes || g1.small || g1.n_jb != 1 || !g2.tile_bytes || g2.small != 2) return false;
+  if (!g1.tile_bytes || g1.small || g1.codes_global || g1.n_jb != 1 || !g2.tile_bytes || g2.small != 2) return false;
   if (L1->in_dim > kFp32MaxD || L2->in_dim != L1->col1 - L1->col0 || L2->col1 - L2->col0 > 8) return false;
   if (L1->scheme != L2->scheme || L1->value_repr != L2->value_repr || L1->oob_policy != L2->oob_policy) return false;
   return tiled_smem(L1, kW, kR) + kMaxKT * 16 + ((g2.tile_bytes + 15) & ~15) <= 227 * 1024;
@@ -827,11 +835,28 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   const bool zs = L->oob_policy == LKG_OOB_ZERO_SPLINE;
   const int W = f64 ? kW64 : kW, R = f64 ? kR64 : kR;
   const int64_t row_tile = (int64_t)W * 32 * R;
-  a.n_items = ((rows + row_tile - 1) / row_tile) * gm.n_jb;
+  a.n_rt = (rows + row_tile - 1) / row_tile;
+  a.n_items = a.n_rt * gm.n_jb;
   const int grid = (int)std::min<int64_t>(a.n_items, sm_count(ctx->device));
   size_t smem = tiled_smem(L, W, R);
   const int sel = (asym << 2) | (sr << 1) | (int)zs;
   static const char* exp_cfg = getenv("LKG_TILED_CFG");  // tuning experiments (sym, spline_component, clip_x)
+  if (gm.codes_global) {
+    switch (sel) {
+#define CASE(S)                                                                                                \
+  case S:                                                                                                      \
+    if (f64)                                                                                                   \
+      launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, true>(ctx->stream, a, smem, grid); \
+    else                                                                                                       \
+      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, true>(ctx->stream, a, smem, grid);    \
+    break;
+      CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+    }
+    LKG_CUDA(cudaGetLastError());
+    ctx->launches++;
+    return;
+  }
   if (exp_cfg && !L2 && !f64 && sel == 2) {
     int ew = 16, er = 2, eb = 1;
     sscanf(exp_cfg, "%d,%d,%d", &ew, &er, &eb);

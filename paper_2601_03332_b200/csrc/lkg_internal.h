@@ -59,6 +59,7 @@ struct TileGeom {
   int32_t p_off = 0, q_off = 0, cb_off = 0;  // byte offsets inside a tile
   int32_t p_stride = 0;  // bytes between (k, i_lo) rows of the P block
   int32_t small = 0, MP = 0;  // whole-layer-in-smem layout (m <= 8), MP = padded out_dim
+  int32_t codes_global = 0;   // tiled layout whose code block is read from global/L2 (GC kernel)
 };
 
 }  // namespace lkg
