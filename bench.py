@@ -35,6 +35,7 @@ WORKLOADS = {
     "c2a": (2, 1_000_000, 64, 1, 1, 0),   # configs[1], uint8 asymmetric
     "c3": (3, 262_144, 64, 0, 0, 0),      # configs[2] cell L=64 sym half_open clip_x
     "c4": (4, 65_536, 64, 0, 0, 0),       # configs[3] (row count reduced per step)
+    "c5": (5, 16_384, 128, 1, 1, 1),      # configs[4]: column-sharded over the ranks, NCCL all-gather
 }
 SMEM_PEAK_GBS = 36600.0  # measured conflict-free LDS.128 throughput, tools/microbench (148 SMs)
 BYTES_PER_EE = {0: 6.0, 1: 10.0}  # algorithmic smem bytes per edge-eval
@@ -169,6 +170,85 @@ def cpu_baseline(wl):
             "sample": f"{n} rows of {wl} (reference lut_model_forward_batch, Tier::Optimized, {nthreads} threads)"}
 
 
+def run_c5(args):
+    """configs[4]: [4096,4096,4096], G=16 on [-2,2], L=128 uint8 asymmetric, closed + zero_spline,
+    16,384 rows; every layer column-sharded over the ranks (strong scaling: total work fixed), NCCL
+    all-gather of the hidden activations between layers (lkg_model_forward_sharded)."""
+    import torch
+    import paper_2601_03332_b200 as lk
+    from paper_2601_03332_b200.sharding import ColumnShardedChain, column_bounds, init_nccl
+    rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    cfg, rows, L, scheme, bm, op = WORKLOADS["c5"]
+    dims, G, _, _ = lk.recipe_dims(cfg)
+    stream = torch.cuda.Stream(device=local)
+    torch.cuda.set_stream(stream)
+    eng = lk.Engine(local, stream.cuda_stream)
+    if dist:
+        init_nccl(eng, dist)
+    else:
+        eng.init_nccl(lk.nccl_unique_id(), 1, 0)
+    qc = lk.QuantConfig(L, lk.Scheme(scheme), lk.Dtype(scheme))
+    oob = lk.OobConfig(lk.BoundaryMode(bm), lk.OobPolicy(op))
+    t_c = time.perf_counter()
+    arts = []
+    for l in range(len(dims) - 1):  # one layer's spec at a time: 2.5 GB/world of f64 coefficients
+        spec = lk.recipe_layer(cfg, l, *column_bounds(dims[l + 1], world, rank))
+        arts.append(ColumnShardedChain.compile([spec], [dims[l + 1]], qc, oob, eng, world, rank).layers[0])
+        del spec
+    compile_s = time.perf_counter() - t_c
+    chain = ColumnShardedChain(arts, world, rank, eng)
+    X = torch.from_numpy(lk.recipe_inputs(cfg, 0, rows)).to(f"cuda:{local}")
+    Y = torch.empty((rows, dims[-1] // world), device=f"cuda:{local}")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        chain.forward(X, Y)
+    barrier()
+    n0 = eng.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            _, st = chain.forward(X, Y)
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ee = rows * sum(dims[l] * dims[l + 1] for l in range(len(dims) - 1))
+    if rank == 0:
+        achieved = ee / world * BYTES_PER_EE[scheme] / (ms * 1e-3) / 1e9
+        line = {"metric": "LUT-KAN forward edge-evals/s (batch x sum d*m)", "value": ee / (ms * 1e-3),
+                "unit": "edge-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "u8 codes, fp32 math, f64 accumulation", "data": "synthetic (BASELINE.json recipe)",
+                "config": {"workload": "c5", "cfg": "configs[4]", "dims": dims, "G": G, "L": L,
+                           "scheme": "uint8_asymmetric", "boundary_mode": "closed", "oob_policy": "zero_spline",
+                           "rows": rows, "parallelism": f"output-column shards x{world}, NCCL all-gather"},
+                "roofline": {"bound": "smem", "achieved": achieved, "peak": SMEM_PEAK_GBS, "unit": "GB/s",
+                             "frac": achieved / SMEM_PEAK_GBS, "traffic": ncu_traffic("c5/layer0"),
+                             "kernel": "per-rank step (2 column-shard layer forwards + all-gather)"},
+                "e2e": None, "gpu_launches": eng.launch_count - n0, "clocks": clk.summary(),
+                "compile": {"gpu_s": compile_s, "note": "host recipe generation + device compile, this rank"},
+                "oob_any_frac_layer0": st[0].oob_any_frac()}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -182,6 +262,9 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args, args.workload)
+        return
+    if args.workload == "c5":
+        run_c5(args)
         return
 
     import torch
@@ -202,7 +285,10 @@ def main():
     eng = lk.Engine(local, stream.cuda_stream)
     qc = lk.QuantConfig(L, lk.Scheme(scheme), lk.Dtype(scheme))
     oob = lk.OobConfig(lk.BoundaryMode(bm), lk.OobPolicy(op))
-    chain = [lk.compile_layer(lk.recipe_layer(cfg, l), qc, oob, engine=eng) for l in range(nl)]
+    specs = [lk.recipe_layer(cfg, l) for l in range(nl)]
+    t_c = time.perf_counter()
+    chain = [lk.compile_layer(s, qc, oob, engine=eng) for s in specs]
+    compile_ms = (time.perf_counter() - t_c) * 1e3
     dev = [a.device(eng) for a in chain]
     import ctypes as C
     from paper_2601_03332_b200._capi import OobStatsC, lib
@@ -319,7 +405,9 @@ def main():
                            "rows_per_gpu": rows, "parallelism": f"batch dp{world}, LUT replicated",
                            "l2": "inputs larger than L2 (no flush)"},
                 "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
-                "oob_any_frac_layer0": stats[0].oob_any_frac(), "clocks": clk.summary()}
+                "oob_any_frac_layer0": stats[0].oob_any_frac(), "clocks": clk.summary(),
+                "compile": {"gpu_ms": compile_ms, "layers": nl,
+                            "note": "lkg_compile_layer for every layer incl. host basis tables and tile build"}}
         if not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline(args.workload)

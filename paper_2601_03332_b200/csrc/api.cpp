@@ -305,7 +305,10 @@ lkg_status lkg_layer_download(lkg_ctx* ctx, const lkg_layer* L, float* knots, ui
     cudaStream_t st = ctx->stream;
     const int64_t E = (int64_t)L->in_dim * L->out_dim;
     if (knots) std::memcpy(knots, L->knots.data(), sizeof(float) * L->knots.size());
-    if (q) LKG_CUDA(cudaMemcpyAsync(q, L->q.p, L->q.bytes, cudaMemcpyDeviceToHost, st));
+    if (q) {
+      if (L->q.p) LKG_CUDA(cudaMemcpyAsync(q, L->q.p, L->q.bytes, cudaMemcpyDeviceToHost, st));
+      else lkg::download_q_from_tiles(ctx, L, q);  // large layers keep their codes only in tiles
+    }
     if (scale) LKG_CUDA(cudaMemcpyAsync(scale, L->scale.p, L->scale.bytes, cudaMemcpyDeviceToHost, st));
     if (y_min) LKG_CUDA(cudaMemcpyAsync(y_min, L->ymin.p, L->ymin.bytes, cudaMemcpyDeviceToHost, st));
     if (L->gains.p) {
@@ -384,7 +387,8 @@ static lkg_status spec_upload_impl(lkg_ctx* ctx, const lkg_spec_desc* d, int32_t
                                  sizeof(double) * m, sizeof(double) * mc, din, cudaMemcpyHostToDevice, st));
     S->col0 = 0;  // device arrays hold only the shard; keep the original range for info
     S->col1 = (int32_t)mc;
-    lkg::launch_spec_prepare(ctx, S.get());
+    // fp32 spline operands are built lazily by the first lkg_spline_forward (saves memory when a
+    // spec is only compiled, e.g. the 33.5M-edge configs[4] layers)
     LKG_CUDA(cudaStreamSynchronize(st));
     *out = S.release();
   });

@@ -89,11 +89,13 @@ struct CompileArgs {
   int32_t K, L, R, W, phi, asym, f16;
 };
 
+constexpr int kCache = 4;  // samples cached per lane (L <= 128 without recomputation)
+
 __device__ __forceinline__ double sample_value(const CompileArgs& a, const double* c, double base,
                                                double spline, double out, int p) {
   const double* b = a.basis + (int64_t)p * a.W;
   const double* cr = c + a.r0[p];
-  double s = 0.0;
+  double s = 0.0;  // starts at +0.0 like the reference (keeps the sign of an all-zero sum)
   for (int t = 0; t < a.W; t++) s = __dadd_rn(s, __dmul_rn(cr[t], b[t]));
   if (!a.phi) return s;
   return __dmul_rn(out, __dadd_rn(__dmul_rn(base, a.silu[p]), __dmul_rn(spline, s)));
@@ -115,8 +117,14 @@ __global__ void __launch_bounds__(256) compile_kernel(CompileArgs a) {
   double amax = 0.0, lo = 0.0, hi = 0.0;
   int lo_i = 0x7fffffff, hi_i = 0x7fffffff;
   bool finite = true;
+  double vc[kCache];  // the lane's samples (L <= 32 * kCache), reused by the code pass
+#pragma unroll
+  for (int t = 0; t < kCache; t++) vc[t] = 0.0;
   for (int l = lane; l < a.L; l += 32) {
     const double v = sample_value(a, c, base, spline, out, p0 + l);
+#pragma unroll
+    for (int t = 0; t < kCache; t++)
+      if (l == lane + 32 * t) vc[t] = v;
     finite = finite && isfinite(v);
     amax = amax < fabs(v) ? fabs(v) : amax;            // std::max(amax, fabs(v))
     if (lo_i == 0x7fffffff || v < lo) { lo = v; lo_i = l; }
@@ -156,12 +164,23 @@ __global__ void __launch_bounds__(256) compile_kernel(CompileArgs a) {
     a.ymin[cell] = (float)ym;
   }
   uint8_t* dst = a.q + cell * a.L;
-  for (int l = lane; l < a.L; l += 32) {
+  // codes_for (compiler.cpp:86-95): round_half_away((v - y_min) / scale). The quotient is
+  // estimated with one reciprocal; round() can only differ from round(correctly rounded quotient)
+  // when the quotient is within a few ulp of a half-integer, so those (rare) cases take the exact
+  // IEEE division. The result is identical to dividing every time.
+  const double inv = sc > 0.0 ? __drcp_rn(sc) : 0.0;
+  for (int l = lane, t = 0; l < a.L; l += 32, t++) {
     int q = 0;
     if (sc > 0.0) {
-      const double v = a.float_table ? a.float_table[cell * a.L + l]
-                                     : sample_value(a, c, base, spline, out, p0 + l);
-      double r = round(__ddiv_rn(__dsub_rn(v, ym), sc));
+      double v = 0.0;
+#pragma unroll
+      for (int tt = 0; tt < kCache; tt++)
+        if (tt == t) v = vc[tt];
+      if (t >= kCache) v = sample_value(a, c, base, spline, out, p0 + l);
+      const double num = __dsub_rn(v, ym);
+      double r = __dmul_rn(num, inv);
+      if (fabs(r - floor(r) - 0.5) < 1e-6) r = __ddiv_rn(num, sc);
+      r = round(r);
       r = r < (double)qlo ? (double)qlo : (r > (double)qhi ? (double)qhi : r);
       q = (int)r;
     }

@@ -703,6 +703,50 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
       off, gm.n_ih, d, m, K, Ls, gm.p_off, gm.q_off, gm.cb_off, !asym, sr, asym);
   LKG_CUDA(cudaGetLastError());
   ctx->launches++;
+  // Layers above 2 GB of codes (configs[3]/[4]) keep their codes only in the tiles; the reference
+  // layout is rebuilt from the tiles on download (download_q_from_tiles).
+  const char* lim = getenv("LKG_TILE_ONLY_BYTES");  // test hook: force the tiles-only mode
+  if (L->q.bytes > (lim ? strtoull(lim, nullptr, 10) : (2ull << 30))) {
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    L->q.release();
+  }
+}
+
+// Tiles -> reference q layout for input rows [i0, i1) (inverse of build_tiles_kernel's code scatter).
+__global__ void tiles_to_q_kernel(const uint8_t* tiles, int64_t tile_bytes, int32_t n_ih, int32_t i0, int32_t i1,
+                                  int32_t m, int32_t K, int32_t L, int sym, uint8_t* q) {
+  const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // cell within the chunk
+  const int64_t n = (int64_t)(i1 - i0) * m * K;
+  if (cell >= n) return;
+  const int64_t e = cell / K;
+  const int k = (int)(cell - e * K);
+  const int i = i0 + (int)(e / m), j = (int)(e % m);
+  const uint8_t* t = tiles + ((int64_t)(j / JB) * n_ih + i / G) * tile_bytes;
+  for (int l = 0; l < L; l++) {
+    const uint8_t b = t[(k * L + l) * LINE + (i % G) * JB + (j % JB)];
+    q[cell * L + l] = sym ? (uint8_t)(b ^ 0x80u) : b;
+  }
+}
+
+void download_q_from_tiles(lkg_ctx* ctx, const lkg_layer* L, uint8_t* host_q) {
+  const TileGeom& gm = L->geom;
+  if (!L->tiles.p || gm.small) throw Error{LKG_ERR_INVALID_ARG, "layer has no code tiles"};
+  const int m = L->col1 - L->col0;
+  const int64_t row_bytes = (int64_t)m * L->K * L->L;
+  const int rows_per_chunk = (int)std::max<int64_t>(1, (256ll << 20) / row_bytes);
+  DBuf tmp;
+  tmp.alloc((size_t)rows_per_chunk * row_bytes);
+  for (int i0 = 0; i0 < L->in_dim; i0 += rows_per_chunk) {
+    const int i1 = std::min(L->in_dim, i0 + rows_per_chunk);
+    const int64_t cells = (int64_t)(i1 - i0) * m * L->K;
+    tiles_to_q_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(
+        L->tiles.as<uint8_t>(), gm.tile_bytes, gm.n_ih, i0, i1, m, L->K, L->L, L->scheme == LKG_SCHEME_SYMMETRIC,
+        tmp.as<uint8_t>());
+    LKG_CUDA(cudaGetLastError());
+    LKG_CUDA(cudaMemcpyAsync(host_q + (int64_t)i0 * row_bytes, tmp.p, (size_t)(i1 - i0) * row_bytes,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  LKG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 // Per-layer coordinate constants (coords.cuh), from the artifact's f32 knots.

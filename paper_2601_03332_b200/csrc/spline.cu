@@ -138,6 +138,7 @@ void launch_spline(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows
   a.X = X;
   a.rows = rows;
   a.Y = Y;
+  if (!S->coeffs32.p) launch_spec_prepare(ctx, const_cast<lkg_spec*>(S));
   a.coeffs = S->coeffs32.as<float>();
   a.cbcs = S->gains32.as<float>();
   a.d = S->in_dim;

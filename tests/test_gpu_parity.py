@@ -63,6 +63,21 @@ def test_compile_large_edge_slices(lk, oracle):
         assert _bytes_equal(g.scale[i * m * K:(i + 1) * m * K], o.scale)
 
 
+def test_compile_tiles_only_download(lk, oracle, monkeypatch):
+    """Large layers keep their codes only in the forward tiles (the reference-layout copy is
+    freed); download rebuilds q_table from the tiles byte for byte. Forced here on a C3 layer."""
+    monkeypatch.setenv("LKG_TILE_ONLY_BYTES", "0")
+    for scheme, L in ((0, 64), (1, 128)):
+        spec = lk.recipe_layer(3, 0)
+        g = lk.compile_layer(spec, lk.QuantConfig(L, lk.Scheme(scheme), lk.Dtype(scheme)), lk.OobConfig())
+        o = oracle.compile_layer(to_oracle_spec(spec), L, scheme, 1, 0, 1, 0)
+        assert _bytes_equal(g.q_table, o.q)
+        X = oracle.recipe_inputs(3, 0, 2000)
+        Y, _ = lk.lut_layer_forward_batch(g, X)
+        Yo, _ = oracle.lut_forward(o, X.astype(np.float64))
+        assert_close(Y, Yo, f"tiles-only L{L}")
+
+
 def test_compile_c5_column_shard(lk, oracle):
     """C5 geometry (G=16 on [-2,2], L=128, uint8 asym): a column shard compiled on the GPU
     matches the oracle's compile of the same edges."""
