@@ -258,6 +258,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-spline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -369,6 +370,29 @@ def main():
                 "edge_evals_per_s": ee_k / (ms_k * 1e-3), "share_of_step": min(1.0, ms_k / ms),
                 "hbm_view": {"peak_gbs": 6547.5, "note": "LUT L2/smem-resident; DRAM traffic is X + Y (see traffic)"}}
 
+    # same-backend honest baseline (paper §5.5): the B-spline chain forward on the same GPU and data
+    spline = None
+    if not args.no_spline:
+        sdev = [sp.device(eng) for sp in specs]
+        bufs = [Xd] + [torch.empty((rows, dims[l + 1]), dtype=torch.float32, device=f"cuda:{local}")
+                       for l in range(nl)]
+
+        def spline_step():
+            for l in range(nl):
+                lk.lutkan.check(lib().lkg_spline_forward(eng.handle, sdev[l].handle, C.c_void_p(bufs[l].data_ptr()),
+                                                         rows, C.c_void_p(bufs[l + 1].data_ptr())))
+        spline_step()
+        barrier()
+        ks = max(3, min(args.steps, 20))
+        e0.record(stream)
+        for _ in range(ks):
+            spline_step()
+        e1.record(stream)
+        barrier()
+        ms_s = e0.elapsed_time(e1) / ks
+        spline = {"value": rows * ee_row / (ms_s * 1e-3), "unit": "edge-evals/s", "ms_per_step": ms_s,
+                  "lut_speedup": ms_s / ms, "kernel": "spline_forward (Cox-de Boor, fp32 terms, f64 accumulation)"}
+
     # end to end through the host-buffer entry point
     e2e = None
     if not args.no_e2e:
@@ -406,6 +430,7 @@ def main():
                            "l2": "inputs larger than L2 (no flush)"},
                 "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
                 "oob_any_frac_layer0": stats[0].oob_any_frac(), "clocks": clk.summary(),
+                "spline_baseline": spline,
                 "compile": {"gpu_ms": compile_ms, "layers": nl,
                             "note": "lkg_compile_layer for every layer incl. host basis tables and tile build"}}
         if not args.no_cpu_baseline:

@@ -92,6 +92,9 @@ struct lkg_spec {
   lkg::DBuf gains;     // f64 [3][E] base, spline, out (compile)
   lkg::DBuf coeffs32;  // f32 [i][R][j] transposed for the spline forward
   lkg::DBuf gains32;   // f32 [2][E]: out*base, out*spline
+  lkg::DBuf spline_tiles;  // spline_tiled.cu layout (uniform cubic grids), built lazily
+  int64_t sp_tile_bytes = 0;
+  int32_t sp_n_ih = 0, sp_n_jb = 0;
 };
 
 struct lkg_ctx {
@@ -139,6 +142,7 @@ void launch_fuse_gains(lkg_ctx* ctx, lkg_layer* L);
 void launch_coords(lkg_ctx* ctx, const lkg_layer* L, const float* x, int64_t n, int32_t* in_range, int32_t* k,
                    int32_t* l0);
 void launch_spec_prepare(lkg_ctx* ctx, lkg_spec* S);
+bool launch_spline_tiled(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows, float* Y);
 
 // Host model_gen (model_gen.cpp).
 int recipe_dims(int cfg, int* n_layers, int* dims, int* G, double* lo, double* hi);

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "lkg_internal.h"
 
@@ -130,6 +131,8 @@ void launch_spec_prepare(lkg_ctx* ctx, lkg_spec* S) {
 void launch_spline(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows, float* Y,
                    const float* /*d_ext*/) {
   if (rows <= 0) return;
+  static const bool force_simple = getenv("LKG_SPLINE_SIMPLE") != nullptr;  // test hook
+  if (!force_simple && launch_spline_tiled(ctx, S, X, rows, Y)) return;
   std::vector<double> ext;
   knot_grid(S->breakpoints, S->degree, ext);
   if ((int)ext.size() > kMaxT || S->degree > kMaxP)

@@ -228,6 +228,47 @@ def test_spline_forward(lk, oracle, cfg, layer, rows):
     assert_close(Y, Yo, f"spline C{cfg}")
 
 
+def _spline_edge_inputs(spec, rows, seed):
+    """Uniform draws plus every extended knot, its fp32 neighbours and far-outside values."""
+    bp = np.asarray(spec.grid.breakpoints, np.float64)
+    p, hl, hr = spec.grid.degree, bp[1] - bp[0], bp[-1] - bp[-2]
+    ext = np.concatenate([bp[0] - hl * np.arange(p, 0, -1), bp, bp[-1] + hr * np.arange(1, p + 1)]).astype(np.float32)
+    special = np.concatenate([ext, np.nextafter(ext, np.float32(-np.inf)), np.nextafter(ext, np.float32(np.inf)),
+                              np.float32([0.0, -0.0, 1e3, -1e3, 20.0, -20.0])])
+    rng = np.random.default_rng(seed)
+    X = rng.uniform(ext[0] - hl, ext[-1] + hr, size=(rows, spec.in_dim)).astype(np.float32)
+    X.ravel()[: special.size * 7 : 7] = np.resize(special, X.ravel()[: special.size * 7 : 7].size)
+    return X
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_spline_forward_knot_edges(lk, oracle, cfg):
+    """Tiled uniform-cubic path at every extended knot and outside the domain (basis 0, silu kept)."""
+    spec = lk.recipe_layer(cfg, 0)
+    X = _spline_edge_inputs(spec, 3000, 50 + cfg)
+    Y = lk.layer_forward_batch(spec, X)
+    Yo = oracle.spline_forward(to_oracle_spec(spec), X.astype(np.float64))
+    assert_close(Y, Yo, f"spline edges C{cfg}")
+
+
+@pytest.mark.parametrize("kind", ["nonuniform", "degree2", "degree5"])
+def test_spline_forward_generic(lk, oracle, kind):
+    """Grids outside the tiled kernel's domain (non-uniform knots, degree != 3): generic kernel."""
+    import dataclasses
+    base = lk.recipe_layer(1, 0)
+    rng = np.random.default_rng(7)
+    bp = np.asarray(base.grid.breakpoints, np.float64).copy()
+    deg = {"nonuniform": 3, "degree2": 2, "degree5": 5}[kind]
+    if kind == "nonuniform":
+        bp[1:-1] += rng.uniform(-0.3, 0.3, bp.size - 2) * (bp[1] - bp[0])
+    E, R = base.in_dim * base.out_dim, bp.size - 1 + deg
+    spec = dataclasses.replace(base, grid=lk.KnotGrid(bp, deg), coeffs=rng.normal(0, 0.5, (E, R)), _dev={})
+    X = _spline_edge_inputs(spec, 2000, 60 + deg)
+    Y = lk.layer_forward_batch(spec, X)
+    Yo = oracle.spline_forward(to_oracle_spec(spec), X.astype(np.float64))
+    assert_close(Y, Yo, f"spline {kind}")
+
+
 # ------------------------------------------------------------------ KATs / errors
 def _hand(lk, bm, op):
     h = hand_artifact_arrays(bm, op)
