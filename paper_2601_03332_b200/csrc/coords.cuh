@@ -22,6 +22,7 @@ struct CoordConst {
   float lo, hi_clip, inv_h, z_thr;
   int32_t K, L, top_l0;  // (top_l0, top_w1): exact coordinates of x' == hi_clip
   float top_w1;
+  float fast_half;       // lut_coords_fast: 0.5 - (node distance below which the exact path runs)
 };
 
 struct Coord {
@@ -60,6 +61,37 @@ __device__ __forceinline__ Coord lut_coords(const CoordConst& c, const float4* k
   o.k = k;
   o.l0 = l0;
   o.w1 = (w1 + 1.0f) - 1.0f;
+  return o;
+}
+
+// silu(x) = x / (1 + 2^(-x log2 e)) with the flush-to-zero MUFU forms (no denormal guards):
+// relative error ~3e-7; x -> -inf gives -0 (rcp(inf) = 0), x -> +inf gives x.
+__device__ __forceinline__ float silu_fast(float x) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return x * r;
+}
+
+// Fast path of lut_coords for the table walk: the segment from the uniform-grid estimate, with no
+// knot compares, and z from that segment's constants. An estimate can only be off by one within a
+// few fp32 roundings of a knot, where z lands next to a sample node; every coordinate closer than
+// 0.5 - c.fast_half to a node takes the exact path above (a grid that failed the host's uniformity
+// bound has fast_half = -1: always exact). Elsewhere floor(z) has no tie to resolve, so k, l0 and
+// the mask equal the reference's. z is formed as 1 + z so that w1 is a multiple of 2^-23.
+__device__ __forceinline__ Coord lut_coords_fast(const CoordConst& c, const float4* ktab, float x) {
+  const float xp = fminf(fmaxf(x, c.lo), c.hi_clip);
+  const int k = min(__float2int_rd((xp - c.lo) * c.inv_h), c.K - 1);
+  const float4 kt = ktab[k];
+  const float dx = xp - kt.x, z1 = fmaf(dx, kt.z, 1.0f), zf = floorf(z1), w1 = z1 - zf;
+  const bool top = xp == c.hi_clip;  // exact host-side coordinates; dx == 0: z = 0 exactly
+  if (!top && dx != 0.0f && fabsf(w1 - 0.5f) > c.fast_half) return lut_coords(c, ktab, x);
+  Coord o;
+  o.in = c.lo <= x && x <= c.hi_clip;
+  o.xp = xp;
+  o.k = k;
+  o.l0 = top ? c.top_l0 : (int)zf - 1;
+  o.w1 = top ? c.top_w1 : w1;
   return o;
 }
 #endif

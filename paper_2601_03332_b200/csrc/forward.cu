@@ -99,7 +99,7 @@ __global__ void coords_tiled_kernel(const __grid_constant__ CoordArgs c, const f
   __syncthreads();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  const lkg::Coord co = lkg::lut_coords(c.cc, ktab, x[t]);
+  const lkg::Coord co = lkg::lut_coords_fast(c.cc, ktab, x[t]);  // the table walk's own path
   if (in_range) in_range[t] = co.in;
   if (k) k[t] = co.k;
   if (l0) l0[t] = co.l0;

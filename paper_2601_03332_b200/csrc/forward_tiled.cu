@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   constexpr int NS = 2;
   constexpr int ROWS_W = 32 * R;        // rows per warp
   constexpr int XS = ROWS_W + 4;        // padded row stride of the transposed x tile
-  constexpr int NX = 4 * R;             // float2 x loads per lane per tile
+  constexpr int NXL = ROWS_W / 4;        // x elements each lane stages per tile (cp.async)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t tb = a.tile_bytes;
   // GC (codes in global): tiles whose code block exceeds shared memory (K*L large, e.g. configs[4])
@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   // from L2, and items are ordered row-tile fastest so concurrent CTAs share each tile in L2.
   const int64_t so = GC ? a.p_off : 0, sb = tb - so;
   uint8_t* stage = smem;                                                  // NS * sb
-  float* xs = reinterpret_cast<float*>(smem + NS * sb) + warp * G * XS;  // per-warp x tile
-  float4* ktab = reinterpret_cast<float4*>(smem + NS * sb + W * G * XS * 4);
+  float* xsw = reinterpret_cast<float*>(smem + NS * sb) + warp * 2 * G * XS;  // per-warp x tiles (x2)
+  float4* ktab = reinterpret_cast<float4*>(smem + NS * sb + 2 * W * G * XS * 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + kMaxKT);
   float4* ktab2 = reinterpret_cast<float4*>(full + 4);
   uint8_t* lut2 = reinterpret_cast<uint8_t*>(ktab2 + kMaxKT);
@@ -118,8 +118,9 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   const int64_t n_local = a.n_items > blockIdx.x ? (a.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t n_stages = n_local * a.n_ih;
   auto issue = [&](int64_t g) {
-    const int64_t item = blockIdx.x + (g / a.n_ih) * gridDim.x;
-    const int jb = GC ? (int)(item / a.n_rt) : (int)(item % a.n_jb), ih = (int)(g % a.n_ih);
+    const uint32_t gs = (uint32_t)g, item = blockIdx.x + (gs / (uint32_t)a.n_ih) * gridDim.x;
+    const int jb = GC ? (int)(item / (uint32_t)a.n_rt) : (int)(item % (uint32_t)a.n_jb);
+    const int ih = (int)(gs % (uint32_t)a.n_ih);
     const uint8_t* src = a.tiles + ((int64_t)jb * a.n_ih + ih) * tb + so;
     uint8_t* dst = stage + (g % NS) * sb;
     mbar_expect_tx(&full[g % NS], (uint32_t)sb);
@@ -137,21 +138,64 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   const int K = a.cc.K, L = a.cc.L;  // knots are uniformly spaced (tiled_eligible)
   uint32_t oob_inputs = 0, oob_rows = 0, oob2_inputs = 0, oob2_rows = 0;
   bool nonfinite = false, nonfinite2 = false;
+  float nfacc = 0.0f;
   int64_t g = 0;
-  // x staging coordinates of this lane: rows lane/4 + 8t, columns 2*(lane&3) + {0,1}
-  const int xr_row = lane >> 2, xr_col = 2 * (lane & 3);
   const int64_t x_rs = a.x_blk > 0 ? a.x_blk : a.d;  // row stride of the input layout
+  // x tiles (64 rows x 8 inputs per warp) go global -> shared with 4-byte cp.async, transposed to
+  // xs[c][row] (conflict-free for the rotated reads), double-buffered one tile ahead. This lane
+  // stages column (lane & 7) of rows (lane >> 3) + 4t. Cells outside [rows) x [d) are written as
+  // t_0: finite and in range, so they never count as OOB; their P and CB entries are 0.
+  // Row tile of local item li (32-bit division: item counts are far below 2^31).
+  auto row0_of = [&](int64_t li_) -> int64_t {
+    const uint32_t item_ = (uint32_t)(blockIdx.x + li_ * gridDim.x);
+    const uint32_t rt_ = GC ? item_ % (uint32_t)a.n_rt : item_ / (uint32_t)a.n_jb;
+    return (int64_t)rt_ * (W * ROWS_W) + warp * ROWS_W;
+  };
+  auto stage_x = [&](int64_t r0_, int ih_, int buf) {
+    const int c_ = lane & 7, i_ = ih_ * G + c_;
+    float* dst = xsw + buf * G * XS + c_ * XS + (lane >> 3);
+    int64_t col_ = i_;
+    if (a.x_blk > 0) {
+      const int b_ = i_ / a.x_blk;
+      col_ = (int64_t)b_ * a.rows * a.x_blk + (i_ - b_ * a.x_blk);
+    }
+    const float* src = a.X + col_ + (r0_ + (lane >> 3)) * x_rs;
+    const uint32_t sd = lkg::smem_u32(dst);
+    if (ih_ * G + G <= a.d && r0_ + ROWS_W <= a.rows) {  // whole tile inside X
+#pragma unroll
+      for (int t = 0; t < NXL; t++)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sd + 16 * t), "l"(src + (int64_t)(4 * t) * x_rs)
+                     : "memory");
+    } else {
+      const int64_t left = a.rows - r0_ - (lane >> 3);
+      const bool cin = i_ < a.d;
+#pragma unroll
+      for (int t = 0; t < NXL; t++) {
+        if (cin && 4 * t < left)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sd + 16 * t),
+                       "l"(src + (int64_t)(4 * t) * x_rs)
+                       : "memory");
+        else
+          dst[4 * t] = lo;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (n_local > 0) stage_x(row0_of(0), 0, 0);
+  int xbuf = 0;
 
   for (int64_t li = 0; li < n_local; li++) {
-    const int64_t item = blockIdx.x + li * gridDim.x;
-    const int64_t rt = GC ? item % a.n_rt : item / a.n_jb;
-    const int jb = GC ? (int)(item / a.n_rt) : (int)(item % a.n_jb);
+    const uint32_t item = (uint32_t)(blockIdx.x + li * gridDim.x);
+    const int64_t rt = GC ? item % (uint32_t)a.n_rt : item / (uint32_t)a.n_jb;
+    const int64_t row0_next = li + 1 < n_local ? row0_of(li + 1) : 0;
+    const int jb = GC ? (int)(item / (uint32_t)a.n_rt) : (int)(item % (uint32_t)a.n_jb);
     const int cnt = jb == 0;  // OOB statistics are counted once per row (j-block 0)
     const int64_t row0 = rt * (int64_t)(W * ROWS_W) + warp * ROWS_W;
     const int64_t rows_left = a.rows - row0;  // rows of this warp: [0, min(ROWS_W, rows_left))
     float2 acc[R][8];
     double acc64[F64 ? R : 1][F64 ? 16 : 1];
-    uint32_t row_oob = 0;  // bit r: row lane + 32 r saw an OOB coordinate
+    uint32_t row_oob = 0;   // bit r: row lane + 32 r saw an OOB coordinate
+    uint32_t oob_item = 0;  // OOB coordinates of this lane's rows in this item
 #pragma unroll
     for (int r = 0; r < R; r++) {
 #pragma unroll
@@ -160,47 +204,17 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
 #pragma unroll
         for (int q = 0; q < 16; q++) acc64[r][q] = 0.0;
     }
-    float2 xr[NX];
-    // x tile (rows row0.., columns 8*ih..8*ih+7) into registers. Cells outside [rows) x [d) read
-    // as t_0: finite and in range, so they never count as OOB; their P and CB entries are 0.
-#define LOAD_XBLOCK(IH)                                                                   \
-  {                                                                                       \
-    const int i_ = (IH) * G + xr_col;                                                     \
-    int64_t cb_;                                                                          \
-    if (a.x_blk > 0) {                                                                    \
-      const int b_ = ((IH) * G) / a.x_blk;                                                \
-      cb_ = (int64_t)b_ * a.rows * a.x_blk + ((IH) * G - b_ * a.x_blk) + xr_col;           \
-    } else {                                                                              \
-      cb_ = (int64_t)(IH) * G + xr_col;                                                   \
-    }                                                                                     \
-    const float* p_ = a.X + cb_ + (row0 + xr_row) * x_rs;                                 \
-    const bool c0_ = i_ < a.d, c1_ = i_ + 1 < a.d;                                        \
-    _Pragma("unroll") for (int t = 0; t < NX; t++) {                                      \
-      float2 v_ = make_float2(lo, lo);                                                    \
-      if (xr_row + 8 * t < rows_left) {                                                   \
-        const float* q_ = p_ + (int64_t)(8 * t) * x_rs;                                   \
-        if (a.x_vec2 && c1_) {                                                            \
-          v_ = __ldg(reinterpret_cast<const float2*>(q_));                                \
-        } else {                                                                          \
-          if (c0_) v_.x = __ldg(q_);                                                      \
-          if (c1_) v_.y = __ldg(q_ + 1);                                                  \
-        }                                                                                 \
-      }                                                                                   \
-      xr[t] = v_;                                                                         \
-    }                                                                                     \
-  }
-    LOAD_XBLOCK(0);
 
     for (int ih = 0; ih < a.n_ih; ih++, g++) {
-      // stage this warp's x tile transposed: xs[c][row] (conflict-free)
+      // this tile's x block has landed (this lane's copies, then the warp's); prefetch the next
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncwarp();
-#pragma unroll
-      for (int t = 0; t < NX; t++) {
-        xs[xr_col * XS + xr_row + 8 * t] = xr[t].x;
-        xs[(xr_col + 1) * XS + xr_row + 8 * t] = xr[t].y;
-      }
-      __syncwarp();
-      if (ih + 1 < a.n_ih) LOAD_XBLOCK(ih + 1);
+      const float* xs = xsw + xbuf * G * XS;
+      if (ih + 1 < a.n_ih)
+        stage_x(row0, ih + 1, xbuf ^ 1);
+      else if (li + 1 < n_local)
+        stage_x(row0_next, 0, xbuf ^ 1);
+      xbuf ^= 1;
       mbar_wait(&full[g % NS], (uint32_t)((g / NS) & 1));
       const uint8_t* T = stage + (g % NS) * sb - so;  // T + p_off is the staged P block
       const uint8_t* Tcodes = GC ? a.tiles + ((int64_t)jb * a.n_ih + ih) * tb : T;
@@ -224,12 +238,12 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
         for (int r = 0; r < R; r++) {
           const float x = xs[il * XS + lane + 32 * r];
           // ---- steps 1-4 (runtime.cpp:170-190): mask, clip, segment, coordinates (coords.cuh)
-          const lkg::Coord co = lkg::lut_coords(a.cc, ktab, x);
+          const lkg::Coord co = lkg::lut_coords_fast(a.cc, ktab, x);
           const bool in = co.in;
           const int k = co.k, l0 = co.l0;
           const float xp = co.xp, w1 = co.w1;  // w1: multiple of 2^-23 -> exact magic constants
-          nonfinite |= !(fabsf(x) <= 3.402823466e38f);
-          oob_inputs += (uint32_t)(cnt & !in);
+          nfacc = fmaf(x, 0.0f, nfacc);  // NaN once any input is NaN or inf
+          oob_item += (uint32_t)!in;
           row_oob |= (uint32_t)(!in) << r;
           const float w0 = 1.0f - w1;
           const float cA = -fmaf(w0, M, OFF), cB = -w1 * M;
@@ -242,7 +256,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           float bx = 0.0f;
           if (SR) {
             const float xb = ZS ? x : xp;  // clip_x clips the base branch too (runtime.cpp:189)
-            bx = __fdividef(xb, 1.0f + __expf(-xb));
+            bx = lkg::silu_fast(xb);
           }
           const float2 W0 = make_float2(w0, w0), W1 = make_float2(w1, w1);
           const float2 CA = make_float2(cA, cA), CB = make_float2(cB, cB), BX = make_float2(bx, bx);
@@ -289,7 +303,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       __syncthreads();  // every warp is done with this stage buffer
       if (tid == 0 && g + NS < n_stages) issue(g + NS);
     }
-#undef LOAD_XBLOCK
+    if (cnt) oob_inputs += oob_item;
     // epilogue: rows of this lane, 16 outputs of the j-block
     const int j0 = jb * JB;
 #pragma unroll
@@ -314,7 +328,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           for (int i2 = 0; i2 < 16; i2++) {
             if (i2 < a.m) {
               const float h = out[i2];
-              const lkg::Coord c2 = lkg::lut_coords(a.cc2, ktab2, h);
+              const lkg::Coord c2 = lkg::lut_coords_fast(a.cc2, ktab2, h);
               nonfinite2 |= !(fabsf(h) <= 3.402823466e38f);
               oob2_inputs += (uint32_t)!c2.in;
               r_oob2 |= !c2.in;
@@ -322,7 +336,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
               float bx2 = 0.0f;
               if (SR) {
                 const float xb = ZS ? h : c2.xp;
-                bx2 = __fdividef(xb, 1.0f + __expf(-xb));
+                bx2 = lkg::silu_fast(xb);
               }
               const int cell = i2 * K2 + c2.k, l1 = min(c2.l0 + 1, L2 - 1);
               const float* V0 = reinterpret_cast<const float*>(lut2) + (cell * L2 + c2.l0) * MP2;
@@ -368,6 +382,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
     if (orow) atomicAdd(a.counters + 0, orow);
     if (oi) atomicAdd(a.counters + 1, oi);
   }
+  nonfinite |= !(nfacc == 0.0f);
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicExch(a.counters + 2, 1ull);
   if (FUSE) {
     unsigned long long oi2 = oob2_inputs, orow2 = oob2_rows;
@@ -442,7 +457,7 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
         }
         x = __ldg(a.X + off);
       }
-      const lkg::Coord co = lkg::lut_coords(a.cc, ktab, x);
+      const lkg::Coord co = lkg::lut_coords_fast(a.cc, ktab, x);
       nonfinite |= !(fabsf(x) <= 3.402823466e38f);
       oob_inputs += (uint32_t)!co.in;
       any_oob |= !co.in;
@@ -450,7 +465,7 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
       float bx = 0.0f;
       if (SR) {
         const float xb = ZS ? x : co.xp;  // clip_x clips the base branch too (runtime.cpp:189)
-        bx = __fdividef(xb, 1.0f + __expf(-xb));
+        bx = lkg::silu_fast(xb);
       }
       const int cell = i * K + co.k, l1 = min(co.l0 + 1, L - 1);
       const float w1 = co.w1, w0 = 1.0f - w1;
@@ -583,7 +598,7 @@ void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
 namespace lkg {
 
 static constexpr int kW = 16, kR = 2;          // fp32 mode: 16 warps x 64 rows = 1024-row tiles
-static constexpr int kW64 = 8, kR64 = 2;       // f64-flush mode: 8 warps x 64 rows = 512-row tiles
+static constexpr int kW64 = 16, kR64 = 1;      // f64-flush mode: 16 warps x 32 rows = 512-row tiles
 static constexpr int kSmallMaxBytes = 200 * 1024;
 
 bool tiled_eligible(const lkg_layer* L) {
@@ -661,7 +676,7 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
     off += G * PROW;
   }
   off = (off + 127) / 128 * 128;
-  const size_t xs_bytes = (size_t)kW * G * (32 * kR + 4) * 4;
+  const size_t xs_bytes = (size_t)2 * kW * G * (32 * kR + 4) * 4;  // double-buffered x tiles
   gm.codes_global = 2 * off + xs_bytes + kMaxKT * 16 + 32 > 227 * 1024;  // codes stay in global (L2)
   if (gm.codes_global && 2 * (off - gm.p_off) + xs_bytes + kMaxKT * 16 + 32 > 227 * 1024) return;  // generic
   gm.tile_bytes = off;
@@ -743,8 +758,23 @@ void fill_coord_const(const lkg_layer* L, CoordConst& c, float4* ktab) {
     int l0 = (int)std::floor(zz);
     l0 = l0 < 0 ? 0 : (l0 > L->L - 1 ? L->L - 1 : l0);
     c.top_l0 = l0;
-    c.top_w1 = (float)(zz - (double)l0);
+    const float w = l0 >= L->L - 1 ? 0.0f : (float)(zz - (double)l0);
+    c.top_w1 = (w + 1.0f) - 1.0f;  // multiple of 2^-23, as lut_coords returns it
   }
+  // lut_coords_fast: the fp32 segment estimate (x' - t_0) * inv_h carries <= 3 roundings
+  // (<= 3K 2^-24 segments) plus the knots' own deviation from a uniform grid; both become z
+  // distances after scaling by (L-1)/h_k. Coordinates within twice that (plus z_thr) of a node
+  // take the exact path.
+  double dev = 0.0, hmin = 1e300, hmax = 0.0;
+  for (int k = 0; k <= L->K; k++) dev = std::max(dev, std::fabs(((double)L->knots[k] - c.lo) * c.inv_h - k));
+  for (int k = 0; k < L->K; k++) {
+    hmin = std::min(hmin, (double)L->knots[k + 1] - L->knots[k]);
+    hmax = std::max(hmax, (double)L->knots[k + 1] - L->knots[k]);
+  }
+  const double seg = (hi - (double)c.lo) / L->K;
+  const double dz = (dev + 4.0 * L->K * 0x1p-24) * (L->L - 1) * seg / hmin;
+  const double thr = 2.0 * dz + c.z_thr;
+  c.fast_half = (thr < 1.0 / 16 && hmax < 1.01 * hmin) ? (float)(0.5 - thr) : -1.0f;
 }
 
 static int sm_count(int dev) {
@@ -812,7 +842,7 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
 
 static size_t tiled_smem(const lkg_layer* L, int W, int R) {
   const int64_t sb = L->geom.tile_bytes - (L->geom.codes_global ? L->geom.p_off : 0);
-  return 2 * sb + (size_t)W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 32;
+  return 2 * sb + (size_t)2 * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 32;
 }
 
 bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
