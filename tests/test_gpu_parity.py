@@ -98,12 +98,22 @@ def test_segment_index_and_mask_bit_exact(lk, oracle, engine, bm):
     import ctypes as C
     import torch
     from paper_2601_03332_b200._capi import lib
-    for cfg in (3, 5):
+    for cfg, L in ((2, 64), (3, 16), (4, 64), (5, 128)):
         spec = lk.recipe_layer(cfg, 0, 0, 1)
-        g = lk.compile_layer(spec, lk.QuantConfig(128 if cfg == 5 else 16),
+        g = lk.compile_layer(spec, lk.QuantConfig(L),
                              lk.OobConfig(lk.BoundaryMode(bm), lk.OobPolicy.ZeroSpline))
         knots = g.knots
         adv = [knots, np.nextafter(knots, np.float32(np.inf)), np.nextafter(knots, np.float32(-np.inf))]
+        # every sample node z = l of every segment (f64 position rounded to f32) and 3 ulps either
+        # side: where floor(z) in fp32 can disagree with the reference's f64 z
+        kd64 = knots.astype(np.float64)
+        nodes = (kd64[:-1, None] + np.arange(L)[None, :] / (L - 1) * np.diff(kd64)[:, None]).ravel().astype(np.float32)
+        for _ in range(3):
+            adv += [nodes := np.nextafter(nodes, np.float32(np.inf))]
+        nodes = (kd64[:-1, None] + np.arange(L)[None, :] / (L - 1) * np.diff(kd64)[:, None]).ravel().astype(np.float32)
+        adv.append(nodes)
+        for _ in range(3):
+            adv += [nodes := np.nextafter(nodes, np.float32(-np.inf))]
         rng = np.random.default_rng(5)
         x = np.concatenate(adv + [rng.uniform(knots[0] * 1.3, knots[-1] * 1.3, 200000).astype(np.float32)])
         x = x.astype(np.float32)
