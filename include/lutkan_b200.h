@@ -64,6 +64,13 @@ typedef struct {
   uint64_t n_samples, n_oob_samples, n_inputs, n_oob_inputs;
 } lkg_oob_stats;
 
+/* EvalReport accuracy fields, metrics.hpp:52-76 (has_oob = 0: mae_oob/maxabs_oob absent). */
+typedef struct {
+  double mae_inrange, maxabs_inrange, mae_oob, maxabs_oob, oob_any_frac;
+  uint64_t n_samples, n_inrange_evals, n_oob_evals, n_boundary_evals, n_oob_samples;
+  int32_t has_oob;
+} lkg_eval_report;
+
 /* LutLayerArtifact fields (runtime.hpp:31-63), host pointers. Gains are required iff
  * value_repr == spline_component; float_table (debug, [E,K,L] f64) is optional. */
 typedef struct {
@@ -180,6 +187,17 @@ lkg_status lkg_spline_forward(lkg_ctx* ctx, const lkg_spec* spec, const float* X
 /* Same with HOST buffers (H2D of X, kernel, D2H of Y; synchronous). */
 lkg_status lkg_spline_forward_host(lkg_ctx* ctx, const lkg_spec* spec, const float* X_host, int64_t rows,
                                    float* Y_host);
+
+/* ------------------------------------------- accuracy */
+/* eval_accuracy(layer, artifact, X) (metrics.cpp:30-103): |lut_eval_phi - eval_edge_phi| over
+ * every (sample, input, edge), bucketed in-range / OOB / boundary; f64 on the device with the
+ * reference's expressions. spec and layer must be the same (unsharded) shape; X [rows, in_dim]
+ * fp32 DEVICE pointer. Synchronous. NON_FINITE if any input is NaN or inf. */
+lkg_status lkg_eval_accuracy(lkg_ctx* ctx, const lkg_spec* spec, const lkg_layer* layer, const float* X,
+                             int64_t rows, lkg_eval_report* out);
+/* Same with a HOST X buffer. */
+lkg_status lkg_eval_accuracy_host(lkg_ctx* ctx, const lkg_spec* spec, const lkg_layer* layer,
+                                  const float* X_host, int64_t rows, lkg_eval_report* out);
 
 /* ------------------------------------------------ multi-GPU (column shards) */
 /* NCCL communicator for output-column sharding. id: 128 bytes from

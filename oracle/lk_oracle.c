@@ -464,6 +464,107 @@ int ork_eval_phi(const ork_artifact* a, int32_t e, double x, double* value) {
   return OK;
 }
 
+/* ------------------------------------------------------- eval_accuracy */
+typedef struct {
+  const ork_spec* s; const ork_artifact* a; const double* X; const double* T; int nT;
+  double sum_in, max_in, sum_oob, max_oob;
+  uint64_t n_in, n_oob, n_bd, oob_samples;
+  int err;
+  pthread_mutex_t mu;
+} ea_ctx;
+
+/* lut_eval_phi (runtime.cpp:96-120) without the per-call artifact validation. */
+static double phi_of(const ork_artifact* a, int64_t e, double x) {
+  int in, k, l0, l1; double xp, w;
+  coords1(a, x, &in, &xp, &k, &l0, &l1, &w);
+  int64_t cell = e * a->K + k;
+  double v = (1.0 - w) * fetch_cell(a, cell, l0) + w * fetch_cell(a, cell, l1);
+  if (a->oob_policy == 1 && !in) v = 0.0;
+  if (a->value_repr == 0) return v;
+  double bx = silu(a->oob_policy == 0 ? xp : x);
+  return (double)a->out_scale[e] * ((double)a->base_scale[e] * bx + (double)a->spline_scale[e] * v);
+}
+
+/* metrics.cpp:44-84, over rows [r0, r1) */
+static void eval_rows(void* p, int64_t r0, int64_t r1) {
+  ea_ctx* c = (ea_ctx*)p;
+  const ork_spec* s = c->s; const ork_artifact* a = c->a;
+  int d = s->in_dim, m = s->out_dim, R = s->K + s->degree;
+  double lo = (double)a->knots[0], hi = (double)a->knots[a->K];
+  double* basis = (double*)malloc(sizeof(double) * (c->nT + 1));
+  double sum_in = 0, max_in = 0, sum_oob = 0, max_oob = 0;
+  uint64_t n_in = 0, n_oob = 0, n_bd = 0, oob_samples = 0;
+  int err = 0;
+  for (int64_t row = r0; row < r1 && !err; row++) {
+    int any = 0;
+    for (int i = 0; i < d; i++) {
+      double x = c->X[row * d + i];
+      if (!isfinite(x)) { err = NONFINITE; break; }
+      int masked = a->boundary_mode == 0 ? !(lo <= x && x < hi) : !(lo <= x && x <= hi);
+      any |= masked;
+      int interior = lo <= x && x < hi;
+      basis_into(c->T, c->nT, s->degree, x, basis);
+      double base = silu(x);
+      for (int j = 0; j < m; j++) {
+        int64_t e = (int64_t)i * m + j;
+        double sp = 0.0;
+        for (int r = 0; r < R; r++) sp += s->coeffs[e * R + r] * basis[r];
+        double ref = s->out_scale[e] * (s->base_scale[e] * base + s->spline_scale[e] * sp);
+        double err_ = fabs(phi_of(a, e, x) - ref);
+        if (masked) { sum_oob += err_; if (err_ > max_oob) max_oob = err_; n_oob++; }
+        else if (interior) { sum_in += err_; if (err_ > max_in) max_in = err_; n_in++; }
+        else n_bd++;
+      }
+    }
+    if (any) oob_samples++;
+  }
+  free(basis);
+  pthread_mutex_lock(&c->mu);
+  if (err) c->err = err;
+  c->sum_in += sum_in; c->sum_oob += sum_oob;
+  if (max_in > c->max_in) c->max_in = max_in;
+  if (max_oob > c->max_oob) c->max_oob = max_oob;
+  c->n_in += n_in; c->n_oob += n_oob; c->n_bd += n_bd; c->oob_samples += oob_samples;
+  pthread_mutex_unlock(&c->mu);
+}
+
+int ork_eval_accuracy(const ork_spec* s, const ork_artifact* a, const double* X, int64_t rows,
+                      int32_t nthreads, double* acc, uint64_t* counts, int32_t* has_oob) {
+  int st = check_artifact(a);
+  if (st) return st;
+  if ((st = check_spec(s))) return st;
+  if (s->in_dim != a->in_dim || s->out_dim != a->out_dim) return fail(DIMENSION, "layer and artifact shapes differ");
+  int nT = s->K + 1 + 2 * s->degree;
+  double* T = (double*)malloc(sizeof(double) * nT);
+  if ((st = knot_grid(s->breakpoints, s->K, s->degree, T))) { free(T); return st; }
+  ea_ctx c;
+  memset(&c, 0, sizeof(c));
+  c.s = s; c.a = a; c.X = X; c.T = T; c.nT = nT;
+  pthread_mutex_init(&c.mu, NULL);
+  run_rows(eval_rows, &c, rows, nthreads);
+  pthread_mutex_destroy(&c.mu);
+  free(T);
+  if (c.err) return fail(c.err, "non-finite input value");
+  acc[0] = c.n_in ? c.sum_in / (double)c.n_in : 0.0;
+  acc[1] = c.max_in;
+  acc[2] = c.n_oob ? c.sum_oob / (double)c.n_oob : 0.0;
+  acc[3] = c.n_oob ? c.max_oob : 0.0;
+  acc[4] = rows ? (double)c.oob_samples / (double)rows : 0.0;
+  *has_oob = c.n_oob > 0;
+  /* memory_breakdown, metrics.cpp:8-28 */
+  uint64_t E = (uint64_t)a->in_dim * a->out_dim, ps = a->param_dtype ? 2 : 4;
+  counts[0] = c.n_in; counts[1] = c.n_oob; counts[2] = c.n_bd; counts[3] = c.oob_samples;
+  counts[4] = E * a->K * a->L;
+  counts[5] = E * a->K * ps;
+  counts[6] = E * a->K * ps;
+  counts[7] = (uint64_t)(a->K + 1) * 4;
+  counts[8] = a->value_repr ? 3 * E * 4 : 0;
+  counts[9] = counts[4] + counts[5] + counts[6] + counts[7] + counts[8];
+  counts[10] = 4 * E * (uint64_t)(s->K + s->degree + 3);
+  acc[5] = counts[10] ? (double)counts[9] / (double)counts[10] : 0.0;
+  return OK;
+}
+
 typedef struct {
   const ork_artifact* a; const double* X; double* Y; int tier;
   const double* cb; const double* cs; const double* T;

@@ -86,6 +86,15 @@ int ork_coords(const ork_artifact* a, const double* x, int64_t n, uint8_t* in_ra
 int ork_eval_value(const ork_artifact* a, int32_t e, double x, double* value, int32_t* was_oob);
 int ork_eval_phi(const ork_artifact* a, int32_t e, double x, double* value);
 
+/* eval_accuracy + memory_breakdown (metrics.cpp:8-103).
+ * acc    = {mae_inrange, maxabs_inrange, mae_oob, maxabs_oob, oob_any_frac, overhead_ratio}
+ * counts = {n_inrange_evals, n_oob_evals, n_boundary_evals, n_oob_samples, q_table_bytes,
+ *           scale_bytes, y_min_bytes, knots_bytes, edge_scalar_bytes, total_bytes, float_model_bytes}
+ * *has_oob = 1 when the OOB bucket is non-empty (mae_oob/maxabs_oob present).
+ * nthreads > 1 shards rows and merges the partial sums (mae then differs in the last bits). */
+int ork_eval_accuracy(const ork_spec* spec, const ork_artifact* a, const double* X, int64_t rows,
+                      int32_t nthreads, double* acc, uint64_t* counts, int32_t* has_oob);
+
 /* basis_values (spline.cpp:89-94) over KnotGrid(breakpoints, degree). out: [K+degree]. */
 int ork_basis_values(const double* breakpoints, int32_t K, int32_t degree, double x, double* out);
 

@@ -148,6 +148,7 @@ class Oracle:
                                             _f64p, _u64p]
         L.ork_spline_forward.argtypes = [_P(_Spec), _f64p, C.c_int64, C.c_int32, C.c_int32, _f64p]
         L.ork_coords.argtypes = [_P(_Art), _f64p, C.c_int64, _u8p, _f64p, _i32p, _i32p, _i32p, _f64p]
+        L.ork_eval_accuracy.argtypes = [_P(_Spec), _P(_Art), _f64p, C.c_int64, C.c_int32, _f64p, _u64p, _i32p]
         L.ork_eval_value.argtypes = [_P(_Art), C.c_int32, C.c_double, _f64p, _i32p]
         L.ork_eval_phi.argtypes = [_P(_Art), C.c_int32, C.c_double, _f64p]
         L.ork_basis_values.argtypes = [_f64p, C.c_int32, C.c_int32, C.c_double, _f64p]
@@ -212,6 +213,22 @@ class Oracle:
         self._chk(self.lib.ork_spline_forward(C.byref(cs), _ptr(X, _f64p), X.shape[0], tier, nthreads,
                                               _ptr(Y, _f64p)))
         return Y
+
+    def eval_accuracy(self, spec: Spec, a: Artifact, X: np.ndarray, nthreads: int = 1) -> dict:
+        """eval_accuracy + memory_breakdown (metrics.cpp:8-103)."""
+        X = np.ascontiguousarray(X, np.float64)
+        acc = np.zeros(6)
+        cnt = np.zeros(11, np.uint64)
+        has = C.c_int32(0)
+        cs, ac = spec._c(), a._c()
+        self._chk(self.lib.ork_eval_accuracy(C.byref(cs), C.byref(ac), _ptr(X, _f64p), X.shape[0], nthreads,
+                                             _ptr(acc, _f64p), _ptr(cnt, _u64p), C.byref(has)))
+        keys = ("n_inrange_evals", "n_oob_evals", "n_boundary_evals", "n_oob_samples", "q_table_bytes",
+                "scale_bytes", "y_min_bytes", "knots_bytes", "edge_scalar_bytes", "total_bytes", "float_model_bytes")
+        r = dict(mae_inrange=acc[0], maxabs_inrange=acc[1], mae_oob=acc[2] if has.value else None,
+                 maxabs_oob=acc[3] if has.value else None, oob_any_frac=acc[4], overhead_ratio=acc[5])
+        r.update({k: int(v) for k, v in zip(keys, cnt)})
+        return r
 
     def coords(self, a: Artifact, x: np.ndarray):
         x = np.ascontiguousarray(x, np.float64).ravel()

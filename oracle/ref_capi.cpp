@@ -5,6 +5,7 @@
 // function below converts plain arrays into the reference types and calls the
 // reference entry point named in its comment; exceptions map to status codes
 // (types.hpp:11-39 taxonomy).
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -13,6 +14,7 @@
 
 #include "lutkan/compiler.hpp"
 #include "lutkan/float16.hpp"
+#include "lutkan/metrics.hpp"
 #include "lutkan/rng.hpp"
 #include "lutkan/runtime.hpp"
 #include "lutkan/spline.hpp"
@@ -217,6 +219,51 @@ int ork_spline_forward(const ork_spec* s, const double* X, int64_t rows, int32_t
       Matrix Ys = layer_forward_batch(spec, Xs, t);  // spline.cpp:183-187
       std::memcpy(Y + r0 * s->out_dim, Ys.data.data(), sizeof(double) * Ys.data.size());
     });
+  });
+}
+
+int ork_eval_accuracy(const ork_spec* s, const ork_artifact* a, const double* X, int64_t rows,
+                      int32_t nthreads, double* acc, uint64_t* counts, int32_t* has_oob) {
+  return guarded([&] {
+    const KanLayerSpec spec = to_spec(s);
+    const LutLayerArtifact art = to_artifact(a);
+    std::vector<EvalReport> parts(nthreads > 1 ? nthreads : 1);
+    std::vector<std::int64_t> nrows(parts.size(), 0);
+    shard_rows(rows, nthreads, [&](std::int64_t r0, std::int64_t r1, int t) {
+      parts[t] = eval_accuracy(spec, art, to_matrix(X + r0 * s->in_dim, r1 - r0, s->in_dim));  // metrics.cpp:30
+      nrows[t] = r1 - r0;
+    });
+    // merge row shards (one shard: the reference's report unchanged)
+    double sum_in = 0, sum_oob = 0, max_in = 0, max_oob = 0, oob_rows = 0;
+    std::uint64_t n_in = 0, n_oob = 0, n_bd = 0;
+    for (std::size_t t = 0; t < parts.size(); t++) {
+      const EvalReport& r = parts[t];
+      sum_in += r.mae_inrange * static_cast<double>(r.n_inrange_evals);
+      n_in += r.n_inrange_evals;
+      max_in = std::max(max_in, r.maxabs_inrange);
+      if (r.mae_oob) {
+        sum_oob += *r.mae_oob * static_cast<double>(r.n_oob_evals);
+        max_oob = std::max(max_oob, *r.maxabs_oob);
+      }
+      n_oob += r.n_oob_evals;
+      n_bd += r.n_boundary_evals;
+      oob_rows += r.oob_any_frac * static_cast<double>(nrows[t]);
+    }
+    const EvalReport& r0 = parts[0];
+    const bool one = parts.size() == 1;
+    acc[0] = one ? r0.mae_inrange : (n_in ? sum_in / static_cast<double>(n_in) : 0.0);
+    acc[1] = max_in;
+    acc[2] = one ? r0.mae_oob.value_or(0.0) : (n_oob ? sum_oob / static_cast<double>(n_oob) : 0.0);
+    acc[3] = n_oob ? max_oob : 0.0;
+    acc[4] = one ? r0.oob_any_frac : (rows ? oob_rows / static_cast<double>(rows) : 0.0);
+    acc[5] = r0.memory.overhead_ratio;
+    *has_oob = n_oob > 0;
+    const MemoryBreakdown& mb = r0.memory;
+    const std::uint64_t c[11] = {n_in, n_oob, n_bd,
+                                 static_cast<std::uint64_t>(acc[4] * static_cast<double>(rows) + 0.5),
+                                 mb.q_table_bytes, mb.scale_bytes, mb.y_min_bytes, mb.knots_bytes,
+                                 mb.edge_scalar_bytes, mb.total_bytes, mb.float_model_bytes};
+    std::memcpy(counts, c, sizeof(c));
   });
 }
 

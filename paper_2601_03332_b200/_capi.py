@@ -53,6 +53,12 @@ class LayerInfo(C.Structure):
                                          "has_float_table")] + [("device_bytes", C.c_uint64)]
 
 
+class EvalReportC(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("mae_inrange", "maxabs_inrange", "mae_oob", "maxabs_oob", "oob_any_frac")] + \
+               [(n, C.c_uint64) for n in ("n_samples", "n_inrange_evals", "n_oob_evals", "n_boundary_evals",
+                                          "n_oob_samples")] + [("has_oob", C.c_int32)]
+
+
 # name -> (restype, argtypes); the exported C-ABI, one entry per declaration in the header.
 SIGNATURES = {
     "lkg_last_error": (C.c_char_p, []),
@@ -84,6 +90,9 @@ SIGNATURES = {
     "lkg_ctx_collect": (C.c_int, [C.c_void_p, _P(OobStatsC), C.c_int32]),
     "lkg_spline_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "lkg_spline_forward_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "lkg_eval_accuracy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, _P(EvalReportC)]),
+    "lkg_eval_accuracy_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                         _P(EvalReportC)]),
     "lkg_nccl_unique_id": (C.c_int, [_P(C.c_uint8)]),
     "lkg_ctx_init_nccl": (C.c_int, [C.c_void_p, _P(C.c_uint8), C.c_int32, C.c_int32]),
     "lkg_model_forward_sharded": (C.c_int, [C.c_void_p, _P(C.c_void_p), C.c_int32, C.c_void_p, C.c_int64,

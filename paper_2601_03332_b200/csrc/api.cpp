@@ -735,6 +735,75 @@ lkg_status lkg_spline_forward_host(lkg_ctx* ctx, const lkg_spec* S, const float*
   });
 }
 
+// ---------------------------------------------------------------- eval_accuracy
+static void eval_impl(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const float* X, int64_t rows,
+                      lkg_eval_report* out) {
+  // metrics.cpp:32-35
+  if (S->in_dim != L->in_dim || S->col1 - S->col0 != L->col1 - L->col0 || S->col0 != L->col0)
+    fail(LKG_ERR_DIMENSION, "layer and artifact shapes differ");
+  lkg_eval_report r{};
+  r.n_samples = (uint64_t)rows;
+  if (rows > 0) {
+    lkg::DBuf acc;
+    acc.alloc(2 * sizeof(double) + 8 * sizeof(unsigned long long));
+    LKG_CUDA(cudaMemsetAsync(acc.p, 0, acc.bytes, ctx->stream));
+    double* dsum = acc.as<double>();
+    unsigned long long* u = reinterpret_cast<unsigned long long*>(dsum + 2);
+    lkg::launch_eval(ctx, S, L, X, rows, dsum, u);
+    double hs[2];
+    unsigned long long hu[8];
+    LKG_CUDA(cudaMemcpyAsync(hs, dsum, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+    LKG_CUDA(cudaMemcpyAsync(hu, u, sizeof(hu), cudaMemcpyDeviceToHost, ctx->stream));
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hu[6]) fail(LKG_ERR_NON_FINITE, "non-finite input value");
+    double mx[2];
+    memcpy(mx, hu, sizeof(mx));
+    r.n_inrange_evals = hu[2];
+    r.n_oob_evals = hu[3];
+    r.n_boundary_evals = hu[4];
+    r.n_oob_samples = hu[5];
+    r.mae_inrange = hu[2] ? hs[0] / (double)hu[2] : 0.0;
+    r.maxabs_inrange = mx[0];
+    r.has_oob = hu[3] > 0;
+    r.mae_oob = hu[3] ? hs[1] / (double)hu[3] : 0.0;
+    r.maxabs_oob = hu[3] ? mx[1] : 0.0;
+    r.oob_any_frac = (double)hu[5] / (double)rows;
+  }
+  *out = r;
+}
+
+lkg_status lkg_eval_accuracy(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const float* X, int64_t rows,
+                             lkg_eval_report* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(S, "spec");
+    need(L, "layer");
+    need(out, "out");
+    if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
+    if (rows > 0) need(X, "X");
+    DeviceGuard g(ctx->device);
+    eval_impl(ctx, S, L, X, rows, out);
+  });
+}
+
+lkg_status lkg_eval_accuracy_host(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const float* Xh,
+                                  int64_t rows, lkg_eval_report* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(S, "spec");
+    need(L, "layer");
+    need(out, "out");
+    if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
+    if (rows > 0) need(Xh, "X");
+    DeviceGuard g(ctx->device);
+    const size_t xb = sizeof(float) * rows * S->in_dim;
+    ensure(ctx->hostio, xb + 256);
+    float* dX = ctx->hostio.as<float>();
+    if (rows > 0) LKG_CUDA(cudaMemcpyAsync(dX, Xh, xb, cudaMemcpyHostToDevice, ctx->stream));
+    eval_impl(ctx, S, L, dX, rows, out);
+  });
+}
+
 // ---------------------------------------------------------------- multi-GPU
 lkg_status lkg_nccl_unique_id(uint8_t id_out[128]) {
   return guarded([&] {

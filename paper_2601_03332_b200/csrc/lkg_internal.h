@@ -142,6 +142,8 @@ void launch_fuse_gains(lkg_ctx* ctx, lkg_layer* L);
 void launch_coords(lkg_ctx* ctx, const lkg_layer* L, const float* x, int64_t n, int32_t* in_range, int32_t* k,
                    int32_t* l0);
 void launch_spec_prepare(lkg_ctx* ctx, lkg_spec* S);
+void launch_eval(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const float* X, int64_t rows,
+                 double* dsum, unsigned long long* u);
 bool launch_spline_tiled(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows, float* Y);
 
 // Host model_gen (model_gen.cpp).

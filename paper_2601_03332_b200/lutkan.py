@@ -587,6 +587,87 @@ def layer_forward_batch(layer: KanLayerSpec, X, tier: Tier = Tier.Optimized, eng
     return Y
 
 
+# ------------------------------------------------------------------ accuracy (metrics.hpp)
+@dataclass
+class MemoryBreakdown:
+    """metrics.hpp:17-33 — exact byte accounting of an artifact next to its float model."""
+    q_table_bytes: int = 0
+    scale_bytes: int = 0
+    y_min_bytes: int = 0
+    knots_bytes: int = 0
+    edge_scalar_bytes: int = 0
+    total_bytes: int = 0
+    float_model_bytes: int = 0
+    overhead_ratio: float = 0.0
+
+    def q_table_frac(self) -> float:
+        return 0.0 if self.total_bytes == 0 else self.q_table_bytes / self.total_bytes
+
+
+def memory_breakdown(artifact: "LutLayerArtifact", layer: KanLayerSpec) -> MemoryBreakdown:
+    """metrics.cpp:8-28 (host arithmetic on the shapes; no table is downloaded)."""
+    E, K, L = artifact.in_dim * artifact.out_dim, artifact.K, artifact.L
+    ps = 2 if artifact.param_dtype == ParamDtype.F16 else 4
+    m = MemoryBreakdown()
+    m.q_table_bytes = E * K * L
+    m.scale_bytes = E * K * ps
+    m.y_min_bytes = E * K * ps
+    m.knots_bytes = (K + 1) * 4
+    m.edge_scalar_bytes = 3 * E * 4 if artifact.value_repr == ValueRepr.SplineComponent else 0
+    m.total_bytes = m.q_table_bytes + m.scale_bytes + m.y_min_bytes + m.knots_bytes + m.edge_scalar_bytes
+    m.float_model_bytes = 4 * layer.in_dim * layer.out_dim * (layer.grid.K + layer.grid.degree + 3)
+    m.overhead_ratio = 0.0 if m.float_model_bytes == 0 else m.total_bytes / m.float_model_bytes
+    return m
+
+
+@dataclass
+class EvalReport:
+    """metrics.hpp:49-76. mae_oob / maxabs_oob are None when the OOB bucket is empty."""
+    quant: QuantConfig
+    oob: OobConfig
+    seed: int = 0
+    n_samples: int = 0
+    mae_inrange: float = 0.0
+    maxabs_inrange: float = 0.0
+    mae_oob: float | None = None
+    maxabs_oob: float | None = None
+    oob_any_frac: float = 0.0
+    n_inrange_evals: int = 0
+    n_oob_evals: int = 0
+    n_boundary_evals: int = 0
+    memory: MemoryBreakdown = field(default_factory=MemoryBreakdown)
+
+
+def eval_accuracy(layer: KanLayerSpec, artifact: "LutLayerArtifact", X, engine: Engine | None = None) -> EvalReport:
+    """metrics.cpp:30-103 on the GPU (csrc/eval.cu): |LUT - spline| per (sample, input, edge) in f64."""
+    eng = engine or default_engine()
+    if layer.in_dim != artifact.in_dim or layer.out_dim != artifact.out_dim:
+        raise DimensionError("layer and artifact shapes differ")
+    if layer.base_kind != "silu":
+        raise UnsupportedBaseError(f'unsupported base kind: "{layer.base_kind}"')
+    spec, dl = layer.device(eng), artifact.device(eng)
+    r = _capi.EvalReportC()
+    if _is_torch(X):
+        if X.dim() != 2 or X.shape[1] != layer.in_dim:
+            raise DimensionError("input column count does not match in_dim")
+        X = X.contiguous().float()
+        check(lib().lkg_eval_accuracy(eng.handle, spec.handle, dl.handle, C.c_void_p(X.data_ptr()), X.shape[0],
+                                      C.byref(r)))
+    else:
+        X = np.asarray(X)
+        if X.ndim != 2 or X.shape[1] != layer.in_dim:
+            raise DimensionError("input column count does not match in_dim")
+        X = np.ascontiguousarray(X, np.float32)
+        check(lib().lkg_eval_accuracy_host(eng.handle, spec.handle, dl.handle, X.ctypes.data_as(C.c_void_p),
+                                           X.shape[0], C.byref(r)))
+    q = QuantConfig(artifact.L, artifact.scheme, artifact.dtype, artifact.value_repr, artifact.interp,
+                    artifact.param_dtype)
+    return EvalReport(q, artifact.oob, 0, int(r.n_samples), r.mae_inrange, r.maxabs_inrange,
+                      r.mae_oob if r.has_oob else None, r.maxabs_oob if r.has_oob else None, r.oob_any_frac,
+                      int(r.n_inrange_evals), int(r.n_oob_evals), int(r.n_boundary_evals),
+                      memory_breakdown(artifact, layer))
+
+
 # ------------------------------------------------------------------ recipes
 def recipe_dims(cfg: int):
     nl, G = C.c_int32(), C.c_int32()

@@ -7,6 +7,7 @@ It loads oracle/_ref/liblutkan_ref.so — the reference's own sources compiled i
   * SHA-256 digests of compiled q_table / scale / y_min bytes (compile_layer),
   * SHA-256 digests of lut_layer_forward_batch / lut_model_forward_batch outputs (f64
     bits) and OobStats, and of layer_forward_batch (spline) outputs,
+  * eval_accuracy reports (metrics.cpp), exact f64 values as hex,
   * a few explicit values for readability.
 tests/test_oracle.py checks the plain-C restatement (oracle/lk_oracle.c) against these
 digests, so the port is pinned to the reference even where /root/reference is absent.
@@ -73,6 +74,16 @@ def main():
         Y, st = o.lut_model_forward(chain, X)
         out["cases"].append(dict(cfg=cfg, chain=True, L=L, scheme=scheme, boundary_mode=bm, oob_policy=op, rows=rows,
                                  y=sha(Y), stats=st.astype(int).tolist(), argmax=sha(np.argmax(Y, 1).astype(np.int64))))
+    # eval_accuracy (metrics.cpp:30-103): exact values (f64 repr) on C1 / C3 cells
+    out["eval"] = []
+    for cfg, rows, L, scheme, bm, op, vr in ((1, 512, 64, 0, 0, 0, 1), (1, 512, 16, 1, 1, 1, 1), (3, 128, 16, 0, 1, 0, 1),
+                                             (3, 128, 32, 1, 0, 1, 1), (3, 128, 16, 1, 1, 1, 0)):
+        spec = o.recipe_layer(cfg, 0)
+        art = o.compile_layer(spec, L, scheme, vr, 0, bm, op)
+        X = o.recipe_inputs(cfg, 0, rows).astype(np.float64)
+        r = o.eval_accuracy(spec, art, X)
+        out["eval"].append(dict(cfg=cfg, rows=rows, L=L, scheme=scheme, boundary_mode=bm, oob_policy=op, value_repr=vr,
+                                report={k: (float(v).hex() if isinstance(v, float) else v) for k, v in r.items()}))
     # rng / input streams
     out["rng"] = dict(normal_7=sha(o.rng_normal(7, 1000)), uniform_7=sha(o.rng_uniform(7, 1000)),
                       inputs={str(c): sha(o.recipe_inputs(c, 0, 64)) for c in (1, 2, 3, 4, 5)})

@@ -279,6 +279,61 @@ def test_spline_forward_generic(lk, oracle, kind):
     assert_close(Y, Yo, f"spline {kind}")
 
 
+# ------------------------------------------------------------------ eval_accuracy (§8f)
+def _eval_match(r, ro, what):
+    """Counts and fractions exact; maxima to f64 rounding; means to summation order."""
+    for k in ("n_inrange_evals", "n_oob_evals", "n_boundary_evals"):
+        assert getattr(r, k) == ro[k], (what, k, getattr(r, k), ro[k])
+    assert r.oob_any_frac == ro["oob_any_frac"], what
+    assert (r.mae_oob is None) == (ro["mae_oob"] is None), what
+    pairs = [(r.maxabs_inrange, ro["maxabs_inrange"]), (r.mae_inrange, ro["mae_inrange"])]
+    if ro["mae_oob"] is not None:
+        pairs += [(r.maxabs_oob, ro["maxabs_oob"]), (r.mae_oob, ro["mae_oob"])]
+    for g, o in pairs:
+        assert abs(g - o) <= 1e-15 + 1e-9 * abs(o), (what, g, o)
+    m = r.memory
+    assert [m.q_table_bytes, m.scale_bytes, m.y_min_bytes, m.knots_bytes, m.edge_scalar_bytes, m.total_bytes,
+            m.float_model_bytes] == [ro[k] for k in ("q_table_bytes", "scale_bytes", "y_min_bytes", "knots_bytes",
+                                                     "edge_scalar_bytes", "total_bytes", "float_model_bytes")], what
+    assert m.overhead_ratio == ro["overhead_ratio"], what
+
+
+@pytest.mark.parametrize("cfg,L,scheme,bm,op,vr,pd,rows", [
+    (1, 64, 0, 0, 0, 1, 0, 4096), (1, 16, 1, 1, 1, 1, 0, 4096), (1, 64, 0, 1, 0, 0, 0, 4096),
+    (2, 64, 0, 1, 0, 1, 0, 3000), (2, 64, 1, 1, 0, 1, 1, 3000),
+    (3, 16, 0, 1, 0, 1, 0, 2000), (3, 128, 1, 0, 1, 1, 0, 2000), (3, 32, 1, 1, 1, 0, 1, 2000)])
+def test_eval_accuracy_gpu(lk, oracle, cfg, L, scheme, bm, op, vr, pd, rows):
+    """GPU eval_accuracy (csrc/eval.cu) vs the reference's metrics.cpp:30-103 on the same inputs
+    (C3 inputs include exact knot values: boundary bucket under closed mode)."""
+    spec = lk.recipe_layer(cfg, 0)
+    so = to_oracle_spec(spec)
+    ao = oracle.compile_layer(so, L, scheme, vr, pd, bm, op)
+    X = oracle.recipe_inputs(cfg, 0, rows)
+    r = lk.eval_accuracy(spec, to_product_artifact(lk, ao), X)
+    ro = oracle.eval_accuracy(so, ao, X.astype(np.float64), nthreads=8)
+    _eval_match(r, ro, f"eval C{cfg} L{L} s{scheme} bm{bm} op{op} vr{vr} pd{pd}")
+    assert r.n_samples == rows and r.quant.samples_per_segment == L
+
+
+def test_eval_accuracy_gpu_float_table_and_errors(lk, oracle):
+    """Debug float_table artifacts (fetch_cell reads the f64 table), hidden-layer inputs,
+    shape mismatch (DimensionError) and non-finite inputs (NonFiniteError)."""
+    spec = lk.recipe_layer(2, 1)
+    so = to_oracle_spec(spec)
+    ao = oracle.compile_layer(so, 32, 0, 1, 0, 1, 1, keep_float=True)
+    X = hidden_inputs(2, 1, 5000, spec.in_dim, -1.6, 1.6)
+    _eval_match(lk.eval_accuracy(spec, to_product_artifact(lk, ao), X),
+                oracle.eval_accuracy(so, ao, X.astype(np.float64), nthreads=8), "float_table")
+    a = to_product_artifact(lk, ao)
+    with pytest.raises(lk.DimensionError):
+        lk.eval_accuracy(lk.recipe_layer(2, 0), a, X)
+    X[3, 2] = np.nan
+    with pytest.raises(lk.NonFiniteError):
+        lk.eval_accuracy(spec, a, X)
+    r = lk.eval_accuracy(spec, a, X[:0])
+    assert r.n_samples == 0 and r.n_inrange_evals == 0 and r.mae_oob is None
+
+
 # ------------------------------------------------------------------ KATs / errors
 def _hand(lk, bm, op):
     h = hand_artifact_arrays(bm, op)

@@ -114,6 +114,20 @@ def test_port_equals_reference_randomized(port, ref, seed):
                         assert np.array_equal(ya, yb) and np.array_equal(sa, sb)
     for tier in (0, 1):
         assert np.array_equal(port.spline_forward(spec, X, tier), ref.spline_forward(spec, X, tier))
+    for vr in (0, 1):  # eval_accuracy (metrics.cpp:30-103), one thread: identical reports
+        a = port.compile_layer(spec, 9, seed % 2, vr, 0, seed % 2, (seed // 2) % 2)
+        assert port.eval_accuracy(spec, a, X) == ref.eval_accuracy(spec, a, X)
+
+
+def test_port_matches_reference_eval_golden(port, golden):
+    """eval_accuracy + memory_breakdown against the reference's reports (exact f64 values)."""
+    assert len(golden["eval"]) >= 5
+    for c in golden["eval"]:
+        spec = port.recipe_layer(c["cfg"], 0)
+        art = port.compile_layer(spec, c["L"], c["scheme"], c["value_repr"], 0, c["boundary_mode"], c["oob_policy"])
+        r = port.eval_accuracy(spec, art, port.recipe_inputs(c["cfg"], 0, c["rows"]).astype(np.float64))
+        for k, v in c["report"].items():
+            assert r[k] == (float.fromhex(v) if isinstance(v, str) else v), (c, k)
 
 
 def _hand(o, bm, op):
