@@ -44,7 +44,15 @@ typedef enum {
   LKG_ERR_CUDA = 5,
   LKG_ERR_NCCL = 6,
   LKG_ERR_OOM = 7,
-  LKG_ERR_INVALID_ARG = 8
+  LKG_ERR_INVALID_ARG = 8,
+  /* artifact container I/O (artifact_io.hpp:11-52) */
+  LKG_ERR_IO = 9,                /* lutkan::IoError */
+  LKG_ERR_CORRUPT_ARCHIVE = 10,  /* lutkan::CorruptArchiveError */
+  LKG_ERR_CORRUPT_BLOB = 11,     /* lutkan::CorruptBlobError */
+  LKG_ERR_MISSING_KEY = 12,      /* lutkan::MissingKeyError */
+  LKG_ERR_SHAPE = 13,            /* lutkan::ShapeError */
+  LKG_ERR_VERSION = 14,          /* lutkan::VersionError */
+  LKG_ERR_ENUM = 15              /* lutkan::EnumError */
 } lkg_status;
 
 enum { LKG_SCHEME_SYMMETRIC = 0, LKG_SCHEME_ASYMMETRIC = 1 };      /* Scheme */
@@ -187,6 +195,22 @@ lkg_status lkg_spline_forward(lkg_ctx* ctx, const lkg_spec* spec, const float* X
 /* Same with HOST buffers (H2D of X, kernel, D2H of Y; synchronous). */
 lkg_status lkg_spline_forward_host(lkg_ctx* ctx, const lkg_spec* spec, const float* X_host, int64_t rows,
                                    float* Y_host);
+
+/* ------------------------------------ artifact container */
+/* save_artifact (artifact_io.cpp:206-219): the `.lut` ZIP container (format lutkan/1).
+ * mode 0: byte-identical to the reference's file (ZIP64 records only above 4 GiB, an extension);
+ * mode 1: stored (method 0) entries; mode 2: parallel-inflate deflate (independently compressed
+ * segments forming one valid deflate stream, segment index in a central-directory extra field).
+ * The reference reader accepts modes 1 and 2. Column shards cannot be saved (CONFIG). */
+lkg_status lkg_artifact_save(lkg_ctx* ctx, const lkg_layer* layer, const char* path, int32_t mode);
+/* load_artifact (artifact_io.cpp:221-300) straight into a device layer: the same checks in the
+ * same order and the same error classes (IO, CORRUPT_ARCHIVE, CORRUPT_BLOB, MISSING_KEY, SHAPE,
+ * VERSION, ENUM, then finalize's CONFIG/DIMENSION/NON_FINITE); ZIP64 archives accepted. */
+lkg_status lkg_artifact_load(lkg_ctx* ctx, const char* path, lkg_layer** out);
+/* Host-only forms (no GPU needed): save from host arrays (finalize checks first), and the full
+ * load validation of a file without an upload (returns the status load would return). */
+lkg_status lkg_artifact_save_desc(const lkg_layer_desc* desc, const char* path, int32_t mode);
+lkg_status lkg_artifact_check(const char* path);
 
 /* ------------------------------------------- accuracy */
 /* eval_accuracy(layer, artifact, X) (metrics.cpp:30-103): |lut_eval_phi - eval_edge_phi| over

@@ -86,6 +86,13 @@ int ork_coords(const ork_artifact* a, const double* x, int64_t n, uint8_t* in_ra
 int ork_eval_value(const ork_artifact* a, int32_t e, double x, double* value, int32_t* was_oob);
 int ork_eval_phi(const ork_artifact* a, int32_t e, double x, double* value);
 
+/* Artifact container (artifact_io.cpp:206-300). REFERENCE LIBRARY ONLY: the port returns 99
+ * (its pin is tests/golden/*.lut, written by the reference). Status codes 9..15 follow the
+ * IoError family as numbered in include/lutkan_b200.h. load_resave loads path and, when
+ * resave_path != NULL, saves the loaded artifact again (a byte-level round trip). */
+int ork_artifact_save(const ork_artifact* a, const char* path);
+int ork_artifact_load_resave(const char* path, const char* resave_path);
+
 /* eval_accuracy + memory_breakdown (metrics.cpp:8-103).
  * acc    = {mae_inrange, maxabs_inrange, mae_oob, maxabs_oob, oob_any_frac, overhead_ratio}
  * counts = {n_inrange_evals, n_oob_evals, n_boundary_evals, n_oob_samples, q_table_bytes,

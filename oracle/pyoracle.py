@@ -148,6 +148,8 @@ class Oracle:
                                             _f64p, _u64p]
         L.ork_spline_forward.argtypes = [_P(_Spec), _f64p, C.c_int64, C.c_int32, C.c_int32, _f64p]
         L.ork_coords.argtypes = [_P(_Art), _f64p, C.c_int64, _u8p, _f64p, _i32p, _i32p, _i32p, _f64p]
+        L.ork_artifact_save.argtypes = [_P(_Art), C.c_char_p]
+        L.ork_artifact_load_resave.argtypes = [C.c_char_p, C.c_char_p]
         L.ork_eval_accuracy.argtypes = [_P(_Spec), _P(_Art), _f64p, C.c_int64, C.c_int32, _f64p, _u64p, _i32p]
         L.ork_eval_value.argtypes = [_P(_Art), C.c_int32, C.c_double, _f64p, _i32p]
         L.ork_eval_phi.argtypes = [_P(_Art), C.c_int32, C.c_double, _f64p]
@@ -213,6 +215,16 @@ class Oracle:
         self._chk(self.lib.ork_spline_forward(C.byref(cs), _ptr(X, _f64p), X.shape[0], tier, nthreads,
                                               _ptr(Y, _f64p)))
         return Y
+
+    def artifact_save(self, a: Artifact, path) -> None:
+        """save_artifact (artifact_io.cpp:206-219); reference library only."""
+        ac = a._c()
+        self._chk(self.lib.ork_artifact_save(C.byref(ac), os.fsencode(path)))
+
+    def artifact_load_status(self, path, resave_path=None) -> int:
+        """load_artifact (artifact_io.cpp:221-300): 0 or the error status (9..15 I/O family);
+        resave_path: write the loaded artifact again."""
+        return self.lib.ork_artifact_load_resave(os.fsencode(path), os.fsencode(resave_path) if resave_path else None)
 
     def eval_accuracy(self, spec: Spec, a: Artifact, X: np.ndarray, nthreads: int = 1) -> dict:
         """eval_accuracy + memory_breakdown (metrics.cpp:8-103)."""

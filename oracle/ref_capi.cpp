@@ -12,6 +12,7 @@
 #include <thread>
 #include <vector>
 
+#include "lutkan/artifact_io.hpp"
 #include "lutkan/compiler.hpp"
 #include "lutkan/float16.hpp"
 #include "lutkan/metrics.hpp"
@@ -33,6 +34,27 @@ int guarded(F&& f) {
   try {
     f();
     return 0;
+  } catch (const CorruptArchiveError& e) {  // artifact_io.hpp:11-52, statuses as lutkan_b200.h
+    g_err = e.what();
+    return 10;
+  } catch (const CorruptBlobError& e) {
+    g_err = e.what();
+    return 11;
+  } catch (const MissingKeyError& e) {
+    g_err = e.what();
+    return 12;
+  } catch (const ShapeError& e) {
+    g_err = e.what();
+    return 13;
+  } catch (const VersionError& e) {
+    g_err = e.what();
+    return 14;
+  } catch (const EnumError& e) {
+    g_err = e.what();
+    return 15;
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return 9;
   } catch (const UnsupportedBaseError& e) {
     g_err = e.what();
     return 4;
@@ -219,6 +241,17 @@ int ork_spline_forward(const ork_spec* s, const double* X, int64_t rows, int32_t
       Matrix Ys = layer_forward_batch(spec, Xs, t);  // spline.cpp:183-187
       std::memcpy(Y + r0 * s->out_dim, Ys.data.data(), sizeof(double) * Ys.data.size());
     });
+  });
+}
+
+int ork_artifact_save(const ork_artifact* a, const char* path) {
+  return guarded([&] { save_artifact(to_artifact(a), path); });  // artifact_io.cpp:206-219
+}
+
+int ork_artifact_load_resave(const char* path, const char* resave_path) {
+  return guarded([&] {
+    const LutLayerArtifact a = load_artifact(path);  // artifact_io.cpp:221-300
+    if (resave_path) save_artifact(a, resave_path);
   });
 }
 

@@ -16,6 +16,8 @@ _P = C.POINTER
 f32p, f64p, u8p, i32p = _P(C.c_float), _P(C.c_double), _P(C.c_uint8), _P(C.c_int32)
 
 OK, ERR_CONFIG, ERR_DIMENSION, ERR_NON_FINITE, ERR_UNSUPPORTED_BASE, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_INVALID_ARG = range(9)
+# artifact container I/O (artifact_io.hpp:11-52)
+ERR_IO, ERR_CORRUPT_ARCHIVE, ERR_CORRUPT_BLOB, ERR_MISSING_KEY, ERR_SHAPE, ERR_VERSION, ERR_ENUM = range(9, 16)
 
 
 class LayerDesc(C.Structure):
@@ -90,6 +92,10 @@ SIGNATURES = {
     "lkg_ctx_collect": (C.c_int, [C.c_void_p, _P(OobStatsC), C.c_int32]),
     "lkg_spline_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "lkg_spline_forward_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "lkg_artifact_save": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_int32]),
+    "lkg_artifact_load": (C.c_int, [C.c_void_p, C.c_char_p, _P(C.c_void_p)]),
+    "lkg_artifact_save_desc": (C.c_int, [_P(LayerDesc), C.c_char_p, C.c_int32]),
+    "lkg_artifact_check": (C.c_int, [C.c_char_p]),
     "lkg_eval_accuracy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, _P(EvalReportC)]),
     "lkg_eval_accuracy_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                          _P(EvalReportC)]),

@@ -136,8 +136,8 @@ void validate_desc(const lkg_layer_desc* d) {
     if (!d->edge_base_scale || !d->edge_spline_scale || !d->edge_out_scale)
       fail(LKG_ERR_DIMENSION, "edge scale arrays must have one entry per edge");
     if (!d->base_kind || !*d->base_kind) fail(LKG_ERR_CONFIG, "spline_component artifact needs a base_kind");
-    if (std::strcmp(d->base_kind, "silu") != 0)
-      fail(LKG_ERR_UNSUPPORTED_BASE, std::string("unsupported base kind: \"") + d->base_kind + "\"");
+    // finalize accepts any base kind (runtime.cpp:34); the optimized forward evaluates silu
+    // whatever it names (runtime.cpp:189) and lut_eval_phi rejects unknown kinds (eval_accuracy)
   } else if (d->value_repr == LKG_REPR_PHI) {
     if (d->edge_base_scale || d->edge_spline_scale || d->edge_out_scale)
       fail(LKG_ERR_CONFIG, "phi artifact must not carry edge scale arrays");
@@ -145,6 +145,12 @@ void validate_desc(const lkg_layer_desc* d) {
     fail(LKG_ERR_CONFIG, "unknown value_repr");
   }
 }
+
+}  // namespace
+namespace lkg {
+void validate_layer_desc(const lkg_layer_desc* d) { validate_desc(d); }
+}  // namespace lkg
+namespace {
 
 // Strided column slice: for every input row i, columns [c0, c1) of a [d, m, inner] array.
 template <class T>
@@ -239,6 +245,7 @@ static lkg_status upload_impl(lkg_ctx* ctx, const lkg_layer_desc* d, int32_t col
     L->K = d->K;
     L->L = d->L;
     L->value_repr = d->value_repr;
+    L->base_kind = d->value_repr == LKG_REPR_SPLINE_COMPONENT && d->base_kind ? d->base_kind : "";
     L->scheme = d->scheme;
     L->param_dtype = d->param_dtype;
     L->boundary_mode = d->boundary_mode;
@@ -497,6 +504,7 @@ lkg_status lkg_compile_layer(lkg_ctx* ctx, const lkg_spec* S, const lkg_quant_co
     L->K = K;
     L->L = Ls;
     L->value_repr = qc->value_repr;
+    L->base_kind = qc->value_repr == LKG_REPR_SPLINE_COMPONENT ? "silu" : "";
     L->scheme = qc->scheme;
     L->param_dtype = qc->param_dtype;
     L->boundary_mode = oob->boundary_mode;
@@ -741,6 +749,8 @@ static void eval_impl(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const
   // metrics.cpp:32-35
   if (S->in_dim != L->in_dim || S->col1 - S->col0 != L->col1 - L->col0 || S->col0 != L->col0)
     fail(LKG_ERR_DIMENSION, "layer and artifact shapes differ");
+  if (L->value_repr == LKG_REPR_SPLINE_COMPONENT && L->base_kind != "silu")  // base_fn, spline.cpp:105-108
+    fail(LKG_ERR_UNSUPPORTED_BASE, "unsupported base kind: \"" + L->base_kind + "\"");
   lkg_eval_report r{};
   r.n_samples = (uint64_t)rows;
   if (rows > 0) {

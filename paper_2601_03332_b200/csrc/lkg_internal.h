@@ -72,6 +72,7 @@ struct lkg_layer {
   int32_t col0 = 0, col1 = 0, full_out_dim = 0;  // column shard [col0, col1) of full_out_dim
   int32_t value_repr = 1, scheme = 0, param_dtype = 0, boundary_mode = 1, oob_policy = 0;
   std::vector<float> knots;  // host copy (K+1), fp32
+  std::string base_kind;     // spline_component: as uploaded ("silu" for compiled layers)
   lkg::DBuf q, scale, ymin, gains;  // reference layout: q [E,K,L], scale/ymin [E,K], gains [3][E]
   lkg::DBuf float_table;            // optional [E,K,L] f64
   lkg::DBuf cbcs;                   // fused gains fp32 [2][E]: cb = out*base, cs = out*spline
@@ -142,6 +143,7 @@ void launch_fuse_gains(lkg_ctx* ctx, lkg_layer* L);
 void launch_coords(lkg_ctx* ctx, const lkg_layer* L, const float* x, int64_t n, int32_t* in_range, int32_t* k,
                    int32_t* l0);
 void launch_spec_prepare(lkg_ctx* ctx, lkg_spec* S);
+void validate_layer_desc(const lkg_layer_desc* d);  // finalize checks (runtime.cpp:11-43)
 void launch_eval(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const float* X, int64_t rows,
                  double* dsum, unsigned long long* u);
 bool launch_spline_tiled(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows, float* Y);

@@ -21,6 +21,7 @@ results come back as fp32; ``tier`` is accepted and ignored (one backend).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 
@@ -59,7 +60,38 @@ class NcclError(Error):
     pass
 
 
-_ERRORS = {_capi.ERR_CONFIG: ConfigError, _capi.ERR_DIMENSION: DimensionError,
+class IoError(Error):
+    """artifact_io.hpp:11-52: the container error family."""
+
+
+class CorruptArchiveError(IoError):
+    pass
+
+
+class CorruptBlobError(IoError):
+    pass
+
+
+class MissingKeyError(IoError):
+    pass
+
+
+class ShapeError(IoError):
+    pass
+
+
+class VersionError(IoError):
+    pass
+
+
+class EnumError(IoError):
+    pass
+
+
+_ERRORS = {_capi.ERR_IO: IoError, _capi.ERR_CORRUPT_ARCHIVE: CorruptArchiveError,
+           _capi.ERR_CORRUPT_BLOB: CorruptBlobError, _capi.ERR_MISSING_KEY: MissingKeyError,
+           _capi.ERR_SHAPE: ShapeError, _capi.ERR_VERSION: VersionError, _capi.ERR_ENUM: EnumError,
+           _capi.ERR_CONFIG: ConfigError, _capi.ERR_DIMENSION: DimensionError,
            _capi.ERR_NON_FINITE: NonFiniteError, _capi.ERR_UNSUPPORTED_BASE: UnsupportedBaseError,
            _capi.ERR_CUDA: CudaError, _capi.ERR_NCCL: NcclError, _capi.ERR_OOM: CudaError,
            _capi.ERR_INVALID_ARG: ValueError}
@@ -585,6 +617,44 @@ def layer_forward_batch(layer: KanLayerSpec, X, tier: Tier = Tier.Optimized, eng
     check(lib().lkg_spline_forward_host(eng.handle, spec.handle, X.ctypes.data_as(C.c_void_p), X.shape[0],
                                         Y.ctypes.data_as(C.c_void_p)))
     return Y
+
+
+# ------------------------------------------------------------------ artifact container (artifact_io.hpp)
+def save_artifact(artifact: "LutLayerArtifact", path, engine: Engine | None = None, store: bool = False,
+                  parallel: bool = False) -> None:
+    """artifact_io.cpp:206-219: the `.lut` container, byte-identical to the reference's file (ZIP64
+    records only when a blob or offset needs them). store=True writes stored entries; parallel=True
+    a deflate stream of independently compressed segments that loads on all host threads (both
+    readable by the reference). Device artifacts (compiled / loaded) are written from device
+    memory; host-array artifacts need no GPU."""
+    mode = 1 if store else (2 if parallel else 0)
+    if artifact._origin is None:
+        d, keep = artifact._desc()
+        check(lib().lkg_artifact_save_desc(C.byref(d), os.fsencode(path), mode))
+        return
+    eng = engine or artifact._origin_engine or default_engine()
+    check(lib().lkg_artifact_save(eng.handle, artifact.device(eng).handle, os.fsencode(path), mode))
+
+
+def check_artifact(path) -> None:
+    """Every load_artifact check (artifact_io.cpp:221-300 + finalize) without a device upload;
+    raises the reference's error class."""
+    check(lib().lkg_artifact_check(os.fsencode(path)))
+
+
+def load_artifact(path, engine: Engine | None = None) -> "LutLayerArtifact":
+    """artifact_io.cpp:221-300 straight to device memory; host arrays materialise lazily."""
+    eng = engine or default_engine()
+    h = C.c_void_p()
+    check(lib().lkg_artifact_load(eng.handle, os.fsencode(path), C.byref(h)))
+    dl = DeviceLayer(h)
+    i = dl.info
+    sr = i.value_repr == int(ValueRepr.SplineComponent)
+    a = LutLayerArtifact(i.in_dim, i.out_dim, i.L, ValueRepr(i.value_repr), Scheme(i.scheme), Dtype(i.scheme),
+                         ParamDtype(i.param_dtype), OobConfig(BoundaryMode(i.boundary_mode), OobPolicy(i.oob_policy)),
+                         "silu" if sr else "")
+    a._origin, a._origin_engine = dl, eng
+    return a
 
 
 # ------------------------------------------------------------------ accuracy (metrics.hpp)
