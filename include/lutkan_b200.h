@@ -143,6 +143,8 @@ lkg_status lkg_layer_upload_columns(lkg_ctx* ctx, const lkg_layer_desc* desc, in
 lkg_status lkg_layer_info_get(const lkg_layer* layer, lkg_layer_info* out);
 /* Copies the layer back in the reference layout (sizes from lkg_layer_info: E = in_dim *
  * (col1-col0)). Any output pointer may be NULL. */
+/* The layer's base_kind ("" for phi), valid while the layer lives. */
+const char* lkg_layer_base_kind(const lkg_layer* layer);
 lkg_status lkg_layer_download(lkg_ctx* ctx, const lkg_layer* layer, float* knots, uint8_t* q_table,
                               float* scale, float* y_min, float* edge_base_scale,
                               float* edge_spline_scale, float* edge_out_scale, double* float_table);

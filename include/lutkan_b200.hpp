@@ -8,6 +8,9 @@
 //   lutkan::lut_model_forward_batch(chain, X, t)  ->  lutkan_b200::lut_model_forward_batch(chain, X, t)
 //   lutkan::compile_layer(spec, qc, oob)          ->  lutkan_b200::compile_layer(spec, qc, oob)
 //   lutkan::layer_forward_batch(spec, X, tier)    ->  lutkan_b200::layer_forward_batch(spec, X, tier)
+//   lutkan::eval_accuracy(spec, a, X)             ->  lutkan_b200::eval_accuracy(spec, a, X)
+//   lutkan::save_artifact(a, path)                ->  lutkan_b200::save_artifact(a, path)
+//   lutkan::load_artifact(path)                   ->  lutkan_b200::load_artifact(path)
 //
 // Documented differences: activations cross to the device as fp32 (results are widened back to
 // f64 in the returned Matrix); Tier is accepted and ignored (one backend, no CPU fallback).
@@ -23,7 +26,9 @@
 #include <utility>
 #include <vector>
 
+#include "lutkan/artifact_io.hpp"
 #include "lutkan/compiler.hpp"
+#include "lutkan/metrics.hpp"
 #include "lutkan/runtime.hpp"
 #include "lutkan/spline.hpp"
 #include "lutkan_b200.h"
@@ -39,6 +44,13 @@ inline void check(lkg_status st) {
     case LKG_ERR_DIMENSION: throw lutkan::DimensionError(msg);
     case LKG_ERR_NON_FINITE: throw lutkan::NonFiniteError(msg);
     case LKG_ERR_UNSUPPORTED_BASE: throw lutkan::UnsupportedBaseError(msg);
+    case LKG_ERR_IO: throw lutkan::IoError(msg);  // artifact_io.hpp:11-52
+    case LKG_ERR_CORRUPT_ARCHIVE: throw lutkan::CorruptArchiveError(msg);
+    case LKG_ERR_CORRUPT_BLOB: throw lutkan::CorruptBlobError(msg);
+    case LKG_ERR_MISSING_KEY: throw lutkan::MissingKeyError(msg);
+    case LKG_ERR_SHAPE: throw lutkan::ShapeError(msg);
+    case LKG_ERR_VERSION: throw lutkan::VersionError(msg);
+    case LKG_ERR_ENUM: throw lutkan::EnumError(msg);
     default: throw lutkan::Error("lutkan_b200: " + msg);
   }
 }
@@ -68,6 +80,15 @@ class Context {
       layers_.erase(it);
     }
     layer_fp_[&a] = fp;
+    const lkg_layer_desc d = desc(a);
+    lkg_layer* out = nullptr;
+    check(lkg_layer_upload(ctx_, &d, &out));
+    layers_[&a] = out;
+    return out;
+  }
+
+  // The artifact's arrays as a C-ABI descriptor (host pointers into `a`).
+  static lkg_layer_desc desc(const lutkan::LutLayerArtifact& a) {
     lkg_layer_desc d{};
     d.in_dim = a.in_dim;
     d.out_dim = a.out_dim;
@@ -93,10 +114,7 @@ class Context {
     d.edge_spline_scale = a.edge_spline_scale.empty() ? nullptr : a.edge_spline_scale.data();
     d.edge_out_scale = a.edge_out_scale.empty() ? nullptr : a.edge_out_scale.data();
     d.float_table = a.float_table.empty() ? nullptr : a.float_table.data();
-    lkg_layer* out = nullptr;
-    check(lkg_layer_upload(ctx_, &d, &out));
-    layers_[&a] = out;
-    return out;
+    return d;
   }
 
   // KanLayerSpec (spline.hpp:35-74) -> device spec (same keying as layer()).
@@ -293,6 +311,83 @@ inline lutkan::Matrix layer_forward_batch(const lutkan::KanLayerSpec& spec, cons
   lutkan::Matrix Y(X.rows, static_cast<size_t>(spec.out_dim()));
   for (size_t i = 0; i < y.size(); i++) Y.data[i] = y[i];
   return Y;
+}
+
+// eval_accuracy (metrics.cpp:30-103) on the GPU (f64, the reference's expressions); memory
+// accounting by the reference's own memory_breakdown.
+inline lutkan::EvalReport eval_accuracy(const lutkan::KanLayerSpec& layer, const lutkan::LutLayerArtifact& a,
+                                        const lutkan::Matrix& X, Context& ctx = default_context()) {
+  if (layer.in_dim() != a.in_dim || layer.out_dim() != a.out_dim)
+    throw lutkan::DimensionError("layer and artifact shapes differ");
+  if (X.cols != static_cast<size_t>(layer.in_dim()))
+    throw lutkan::DimensionError("input column count does not match in_dim");
+  std::vector<float> x(X.data.begin(), X.data.end());
+  lkg_eval_report r{};
+  check(lkg_eval_accuracy_host(ctx.get(), ctx.spec(layer), ctx.layer(a), x.data(), static_cast<int64_t>(X.rows), &r));
+  lutkan::EvalReport e;
+  e.quant.samples_per_segment = a.L;
+  e.quant.scheme = a.scheme;
+  e.quant.dtype = a.dtype;
+  e.quant.value_repr = a.value_repr;
+  e.quant.interp = a.interp;
+  e.quant.param_dtype = a.param_dtype;
+  e.oob = a.oob;
+  e.n_samples = X.rows;
+  e.mae_inrange = r.mae_inrange;
+  e.maxabs_inrange = r.maxabs_inrange;
+  if (r.has_oob) {
+    e.mae_oob = r.mae_oob;
+    e.maxabs_oob = r.maxabs_oob;
+  }
+  e.oob_any_frac = r.oob_any_frac;
+  e.n_inrange_evals = r.n_inrange_evals;
+  e.n_oob_evals = r.n_oob_evals;
+  e.n_boundary_evals = r.n_boundary_evals;
+  e.memory = lutkan::memory_breakdown(a, layer);
+  return e;
+}
+
+// save_artifact (artifact_io.cpp:206-219): byte-identical archive.
+inline void save_artifact(const lutkan::LutLayerArtifact& a, const std::string& path) {
+  const lkg_layer_desc d = Context::desc(a);
+  check(lkg_artifact_save_desc(&d, path.c_str(), 0));
+}
+
+// load_artifact (artifact_io.cpp:221-300): parsed, checked and uploaded by the engine (the
+// device copy is what forwards use); the reference's host artifact is returned, finalized.
+inline lutkan::LutLayerArtifact load_artifact(const std::string& path, Context& ctx = default_context()) {
+  lkg_layer* dev = nullptr;
+  check(lkg_artifact_load(ctx.get(), path.c_str(), &dev));
+  std::unique_ptr<lkg_layer, lkg_status (*)(lkg_layer*)> guard(dev, lkg_layer_free);
+  lkg_layer_info info{};
+  check(lkg_layer_info_get(dev, &info));
+  lutkan::LutLayerArtifact a;
+  a.in_dim = info.in_dim;
+  a.out_dim = info.out_dim;
+  a.L = info.L;
+  a.value_repr = static_cast<lutkan::ValueRepr>(info.value_repr);
+  a.scheme = static_cast<lutkan::Scheme>(info.scheme);
+  a.dtype = info.scheme ? lutkan::Dtype::Uint8 : lutkan::Dtype::Int8;
+  a.param_dtype = static_cast<lutkan::ParamDtype>(info.param_dtype);
+  a.oob.boundary_mode = static_cast<lutkan::BoundaryMode>(info.boundary_mode);
+  a.oob.oob_policy = static_cast<lutkan::OobPolicy>(info.oob_policy);
+  const bool sr = a.value_repr == lutkan::ValueRepr::SplineComponent;
+  a.base_kind = lkg_layer_base_kind(dev);
+  const size_t E = static_cast<size_t>(info.in_dim) * info.out_dim, K = info.K;
+  a.knots.resize(K + 1);
+  a.q_table.resize(E * K * a.L);
+  a.scale.resize(E * K);
+  a.y_min.resize(E * K);
+  if (sr) {
+    a.edge_base_scale.resize(E);
+    a.edge_spline_scale.resize(E);
+    a.edge_out_scale.resize(E);
+  }
+  check(lkg_layer_download(ctx.get(), dev, a.knots.data(), a.q_table.data(), a.scale.data(), a.y_min.data(),
+                           sr ? a.edge_base_scale.data() : nullptr, sr ? a.edge_spline_scale.data() : nullptr,
+                           sr ? a.edge_out_scale.data() : nullptr, nullptr));
+  a.finalize();
+  return a;
 }
 
 }  // namespace lutkan_b200

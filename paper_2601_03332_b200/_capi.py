@@ -73,6 +73,7 @@ SIGNATURES = {
     "lkg_layer_upload": (C.c_int, [C.c_void_p, _P(LayerDesc), _P(C.c_void_p)]),
     "lkg_layer_upload_columns": (C.c_int, [C.c_void_p, _P(LayerDesc), C.c_int32, C.c_int32, _P(C.c_void_p)]),
     "lkg_layer_info_get": (C.c_int, [C.c_void_p, _P(LayerInfo)]),
+    "lkg_layer_base_kind": (C.c_char_p, [C.c_void_p]),
     "lkg_layer_download": (C.c_int, [C.c_void_p, C.c_void_p, f32p, u8p, f32p, f32p, f32p, f32p, f32p, f64p]),
     "lkg_layer_free": (C.c_int, [C.c_void_p]),
     "lkg_spec_upload": (C.c_int, [C.c_void_p, _P(SpecDesc), _P(C.c_void_p)]),

@@ -303,6 +303,8 @@ lkg_status lkg_layer_info_get(const lkg_layer* L, lkg_layer_info* o) {
   });
 }
 
+const char* lkg_layer_base_kind(const lkg_layer* L) { return L ? L->base_kind.c_str() : ""; }
+
 lkg_status lkg_layer_download(lkg_ctx* ctx, const lkg_layer* L, float* knots, uint8_t* q, float* scale,
                               float* y_min, float* bs, float* ss, float* os, double* ft) {
   return guarded([&] {

@@ -7,9 +7,14 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <fstream>
+#include <iterator>
+#include <string>
 #include <vector>
 
+#include "lutkan/artifact_io.hpp"
 #include "lutkan/compiler.hpp"
+#include "lutkan/metrics.hpp"
 #include "lutkan/model_gen.hpp"
 #include "lutkan/runtime.hpp"
 #include "lutkan/spline.hpp"
@@ -115,6 +120,50 @@ int main() {
       threw = true;
     }
     CHECK(threw, "non-finite input -> NonFiniteError");
+  }
+  // eval_accuracy and the artifact container through the shim
+  {
+    QuantConfig cfg;
+    cfg.samples_per_segment = 16;
+    const KanLayerSpec layer = gen_layer(7, 9, 6, 5, 3);
+    const OobConfig oob{BoundaryMode::Closed, OobPolicy::ClipX};
+    const LutLayerArtifact art = lutkan::compile_layer(layer, cfg, oob);
+    Matrix X = gen_inputs(19, 500, 9, -1.4, 1.4, false);
+    for (double& v : X.data) v = static_cast<double>(static_cast<float>(v));
+    const EvalReport er = lutkan::eval_accuracy(layer, art, X);
+    const EvalReport eg = lutkan_b200::eval_accuracy(layer, art, X);
+    CHECK(er.n_inrange_evals == eg.n_inrange_evals && er.n_oob_evals == eg.n_oob_evals &&
+              er.n_boundary_evals == eg.n_boundary_evals && er.oob_any_frac == eg.oob_any_frac &&
+              er.mae_oob.has_value() == eg.mae_oob.has_value(),
+          "eval_accuracy buckets and counts identical");
+    CHECK(std::fabs(er.mae_inrange - eg.mae_inrange) <= 1e-12 * er.mae_inrange &&
+              std::fabs(er.maxabs_inrange - eg.maxabs_inrange) <= 1e-15 + 1e-12 * er.maxabs_inrange &&
+              er.memory.total_bytes == eg.memory.total_bytes,
+          "eval_accuracy errors agree (f64)");
+    lutkan::save_artifact(art, "/tmp/shim_ref.lut");
+    lutkan_b200::save_artifact(art, "/tmp/shim_gpu.lut");
+    auto slurp = [](const char* p) {
+      std::ifstream f(p, std::ios::binary);
+      return std::string((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    };
+    CHECK(slurp("/tmp/shim_ref.lut") == slurp("/tmp/shim_gpu.lut"), "save_artifact bytes identical");
+    const LutLayerArtifact back = lutkan_b200::load_artifact("/tmp/shim_ref.lut");
+    const LutLayerArtifact back_ref = lutkan::load_artifact("/tmp/shim_ref.lut");
+    CHECK(back.q_table == back_ref.q_table && back.scale == back_ref.scale && back.knots == back_ref.knots &&
+              back.edge_base_scale == back_ref.edge_base_scale && back.base_kind == back_ref.base_kind,
+          "load_artifact fields identical");
+    {
+      std::ofstream f("/tmp/shim_bad.lut", std::ios::binary);
+      const std::string raw = slurp("/tmp/shim_ref.lut");
+      f << raw.substr(0, raw.size() / 2);
+    }
+    bool threw = false;
+    try {
+      lutkan_b200::load_artifact("/tmp/shim_bad.lut");
+    } catch (const CorruptArchiveError&) {
+      threw = true;
+    }
+    CHECK(threw, "truncated archive -> CorruptArchiveError");
   }
   std::printf("%s: %d failure(s)\n", fails ? "FAILED" : "OK", fails);
   return fails ? 1 : 0;
