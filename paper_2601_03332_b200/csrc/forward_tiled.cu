@@ -677,7 +677,8 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   }
   off = (off + 127) / 128 * 128;
   const size_t xs_bytes = (size_t)2 * kW * G * (32 * kR + 4) * 4;  // double-buffered x tiles
-  gm.codes_global = 2 * off + xs_bytes + kMaxKT * 16 + 32 > 227 * 1024;  // codes stay in global (L2)
+  static const bool force_gc = getenv("LKG_FORCE_GC") != nullptr;  // test / tuning hook
+  gm.codes_global = force_gc || 2 * off + xs_bytes + kMaxKT * 16 + 32 > 227 * 1024;  // codes stay in global (L2)
   if (gm.codes_global && 2 * (off - gm.p_off) + xs_bytes + kMaxKT * 16 + 32 > 227 * 1024) return;  // generic
   gm.tile_bytes = off;
   gm.JB = JB;
@@ -846,6 +847,12 @@ static size_t tiled_smem(const lkg_layer* L, int W, int R) {
 }
 
 bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
+  // Off by default: measured on C2, the fused epilogue (16 coordinates per row at the end of
+  // each item, plus the second layer's state in the main kernel's registers) costs 0.20 ms per
+  // step against 0.07 ms for the separate fwd_small launch (1.59e12 vs 1.88e12 edge-evals/s).
+  // LKG_FUSE=1 re-enables it (kept for the C1-sized chains of SURVEY §8f rank 3).
+  static const char* fz = getenv("LKG_FUSE");
+  if (!fz || fz[0] != '1') return false;
   const TileGeom &g1 = L1->geom, &g2 = L2->geom;
   if (!g1.tile_bytes || g1.small || g1.codes_global || g1.n_jb != 1 || !g2.tile_bytes || g2.small != 2) return false;
   if (L1->in_dim > kFp32MaxD || L2->in_dim != L1->col1 - L1->col0 || L2->col1 - L2->col0 > 8) return false;

@@ -209,11 +209,37 @@ def test_chain_argmax_c2(lk, oracle):
         gap = np.abs(Yo[:, 0] - Yo[:, 1])
         assert np.all(agree | (gap < 1e-4)), (np.sum(~agree), gap[~agree].max())
         assert [stats_list(s) for s in r.per_layer] == sto.astype(int).tolist()
-        # the chain (layer 2 fused into layer 1's epilogue) per layer on the GPU's own hidden values
+        # layer 2 per layer on the GPU's own hidden values
         chain = [to_product_artifact(lk, a) for a in chain_o]
         H, _ = lk.lut_layer_forward_batch(chain[0], X[:5000])
         Y2o, _ = oracle.lut_forward(chain_o[1], H.astype(np.float64))
-        assert_close(r.Y[:5000], Y2o, "C2 fused layer 2")
+        assert_close(r.Y[:5000], Y2o, "C2 layer 2")
+
+
+def test_chain_fused_epilogue(tmp_path):
+    """The epilogue-fused chain (LKG_FUSE=1: layer 2 evaluated in layer 1's epilogue, off by
+    default) gives the unfused chain's outputs and stats, in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = (
+        "import sys, numpy as np; sys.path[:0] = [%r, %r]\n"
+        "import paper_2601_03332_b200 as lk\n"
+        "X = lk.recipe_inputs(2, 0, 20000)\n"
+        "for s in (0, 1):\n"
+        "    ch = lk.compile_model([lk.recipe_layer(2, l) for l in range(2)], lk.QuantConfig(64, lk.Scheme(s), lk.Dtype(s)),"
+        " lk.OobConfig())\n"
+        "    r = lk.lut_model_forward_batch(ch, X)\n"
+        "    np.save(%r + '/y%%d.npy' %% s, r.Y); np.save(%r + '/s%%d.npy' %% s, np.array([[x.n_oob_samples, x.n_oob_inputs]"
+        " for x in r.per_layer]))\n") % (os.path.dirname(here), here, str(tmp_path), str(tmp_path))
+    outs = {}
+    for fuse in ("0", "1"):
+        subprocess.run([sys.executable, "-c", code], env=dict(os.environ, LKG_FUSE=fuse), check=True)
+        outs[fuse] = [(np.load(tmp_path / f"y{s}.npy"), np.load(tmp_path / f"s{s}.npy")) for s in (0, 1)]
+    for (y0, s0), (y1, s1) in zip(outs["0"], outs["1"]):
+        assert np.array_equal(s0, s1)
+        assert np.max(np.abs(y0 - y1)) <= 1e-6
 
 
 def test_chain_c1(lk, oracle):

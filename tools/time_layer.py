@@ -1,5 +1,5 @@
 """Time one layer forward (CUDA events, device-resident X) for kernel tuning experiments.
-Usage: python tools/time_layer.py [workload] [layer] [iters]"""
+Usage: python tools/time_layer.py [workload] [layer] [iters] [L]"""
 import ctypes as C
 import os
 import sys
@@ -15,6 +15,8 @@ wl = sys.argv[1] if len(sys.argv) > 1 else "c2"
 layer = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 50
 cfg, rows, L, scheme, bm, op = WORKLOADS[wl]
+if len(sys.argv) > 4:
+    L = int(sys.argv[4])
 dims, _, _, _ = lk.recipe_dims(cfg)
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
