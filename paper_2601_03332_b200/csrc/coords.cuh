@@ -79,6 +79,25 @@ __device__ __forceinline__ float silu_fast(float x) {
 // 0.5 - c.fast_half to a node takes the exact path above (a grid that failed the host's uniformity
 // bound has fast_half = -1: always exact). Elsewhere floor(z) has no tie to resolve, so k, l0 and
 // the mask equal the reference's. z is formed as 1 + z so that w1 is a multiple of 2^-23.
+// Branch-free half of lut_coords_fast: the fast coordinates and whether the exact path must
+// replace them (lets a caller run several rows' coordinate chains side by side and take the
+// exact path once for all of them).
+__device__ __forceinline__ Coord lut_coords_fast_nb(const CoordConst& c, const float4* ktab, float x, bool& slow) {
+  const float xp = fminf(fmaxf(x, c.lo), c.hi_clip);
+  const int k = min(__float2int_rd((xp - c.lo) * c.inv_h), c.K - 1);
+  const float4 kt = ktab[k];
+  const float dx = xp - kt.x, z1 = fmaf(dx, kt.z, 1.0f), zf = floorf(z1), w1 = z1 - zf;
+  const bool top = xp == c.hi_clip;
+  slow = !top && dx != 0.0f && fabsf(w1 - 0.5f) > c.fast_half;
+  Coord o;
+  o.in = c.lo <= x && x <= c.hi_clip;
+  o.xp = xp;
+  o.k = k;
+  o.l0 = top ? c.top_l0 : (int)zf - 1;
+  o.w1 = top ? c.top_w1 : w1;
+  return o;
+}
+
 __device__ __forceinline__ Coord lut_coords_fast(const CoordConst& c, const float4* ktab, float x) {
   const float xp = fminf(fmaxf(x, c.lo), c.hi_clip);
   const int k = min(__float2int_rd((xp - c.lo) * c.inv_h), c.K - 1);
