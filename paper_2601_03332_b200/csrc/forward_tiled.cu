@@ -458,6 +458,10 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
   const float* CBt = reinterpret_cast<const float*>(lut + a.cb_off);
   uint32_t oob_inputs = 0, oob_rows = 0;
   bool nonfinite = false;
+  float nfacc = 0.0f;
+  // input pairs need 8-byte aligned (i, i+1) in the same row / column block
+  const bool pairs = (d % 2 == 0) && (a.x_blk > 0 ? a.x_blk % 2 == 0 : true) &&
+                     ((reinterpret_cast<uintptr_t>(a.X) & 7) == 0);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t rb = (int64_t)blockIdx.x * blockDim.x; rb < a.rows; rb += stride) {
     const int64_t row = rb + tid;
@@ -466,21 +470,8 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
 #pragma unroll
     for (int j = 0; j < 8; j++) y[j] = 0.0f;
     bool any_oob = false;
-    int i = i0;
-    for (int t = 0; t < d; t++, i = (i + 1 == d) ? 0 : i + 1) {
-      float x = lo;
-      if (vrow) {
-        int64_t off;
-        if (a.x_blk > 0) {
-          const int b = i / a.x_blk;
-          off = (int64_t)b * a.rows * a.x_blk + row * x_rs + (i - b * a.x_blk);
-        } else {
-          off = row * x_rs + i;
-        }
-        x = __ldg(a.X + off);
-      }
-      const lkg::Coord co = lkg::lut_coords_fast(a.cc, ktab, x);
-      nonfinite |= !(fabsf(x) <= 3.402823466e38f);
+    // one input's table walk + base branch for this row (runtime.cpp:192-212)
+    auto accum = [&](int i, float x, const lkg::Coord& co) {
       oob_inputs += (uint32_t)!co.in;
       any_oob |= !co.in;
       const bool tab = !(ZS && !co.in);
@@ -519,6 +510,41 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
           }
         }
       }
+    };
+    auto x_at = [&](int i) -> int64_t {
+      if (a.x_blk > 0) {
+        const int b = i / a.x_blk;
+        return (int64_t)b * a.rows * a.x_blk + row * x_rs + (i - b * a.x_blk);
+      }
+      return row * x_rs + i;
+    };
+    if (pairs) {
+      // inputs in pairs (i even): one 8-byte load, both fast coordinate chains side by side,
+      // the exact path once if either needs it
+      int i = 2 * (lane % (d >> 1));
+      for (int t = 0; t < d; t += 2, i = (i + 2 == d) ? 0 : i + 2) {
+        float2 xx = make_float2(lo, lo);
+        if (vrow) xx = __ldg(reinterpret_cast<const float2*>(a.X + x_at(i)));
+        bool s0, s1;
+        lkg::Coord c0 = lkg::lut_coords_fast_nb(a.cc, ktab, xx.x, s0);
+        lkg::Coord c1 = lkg::lut_coords_fast_nb(a.cc, ktab, xx.y, s1);
+        if (s0 || s1) {
+          if (s0) c0 = lkg::lut_coords(a.cc, ktab, xx.x);
+          if (s1) c1 = lkg::lut_coords(a.cc, ktab, xx.y);
+        }
+        nfacc = fmaf(xx.x, 0.0f, fmaf(xx.y, 0.0f, nfacc));  // NaN once any input is NaN or inf
+        accum(i, xx.x, c0);
+        accum(i + 1, xx.y, c1);
+      }
+    } else {
+      int i = i0;
+      for (int t = 0; t < d; t++, i = (i + 1 == d) ? 0 : i + 1) {
+        float x = lo;
+        if (vrow) x = __ldg(a.X + x_at(i));
+        const lkg::Coord co = lkg::lut_coords_fast(a.cc, ktab, x);
+        nfacc = fmaf(x, 0.0f, nfacc);
+        accum(i, x, co);
+      }
     }
     if (vrow) {
       float* yr = a.Y + row * a.m;
@@ -537,6 +563,7 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
     if (orow) atomicAdd(a.counters + 0, orow);
     if (oi) atomicAdd(a.counters + 1, oi);
   }
+  nonfinite |= !(nfacc == 0.0f);
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicExch(a.counters + 2, 1ull);
 }
 
