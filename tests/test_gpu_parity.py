@@ -431,3 +431,69 @@ def test_errors_and_edges_gpu(lk, oracle):
         lk.layer_forward_batch(s, np.zeros((1, 2), np.float32))
     with pytest.raises(lk.ConfigError):
         lk.compile_layer(lk.recipe_layer(1, 0), lk.QuantConfig(1))
+
+
+# ------------------------------------------------------------------ edge cases / maximum sizes
+def _special_values(knots):
+    k = np.asarray(knots, np.float32)
+    lo, hi = k[0], k[-1]
+    inf, ninf = np.float32(np.inf), np.float32(-np.inf)
+    vals = [0.0, -0.0, 1e-40, -1e-40, 1e-38, 1e30, -1e30, lo, hi,
+            np.nextafter(lo, ninf), np.nextafter(lo, inf), np.nextafter(hi, ninf), np.nextafter(hi, inf)]
+    vals += list(k) + list(np.nextafter(k, inf)) + list(np.nextafter(k, ninf))
+    return np.array(vals, np.float32)
+
+
+@pytest.mark.parametrize("cfg,layer,scheme", [(2, 0, 0), (2, 1, 1), (3, 0, 1), (4, 2, 0)])
+@pytest.mark.parametrize("bm,op", [(0, 0), (0, 1), (1, 0), (1, 1)])
+def test_forward_special_values_ragged_rows(lk, oracle, cfg, layer, scheme, bm, op):
+    """Every knot ±1 ulp, t_0/t_K and their neighbours, ±0, subnormals, ±1e30, ±3e38, scattered
+    through ragged row counts (1, 31, 33, 1025, 2049: partial warps, tiles and row tiles), all
+    four boundary/OOB contracts, tiled (m=16/64/1024) and small (m=2/10) layouts."""
+    spec = oracle.recipe_layer(cfg, layer)
+    art = oracle.compile_layer(spec, 32, scheme, 1, 0, bm, op)
+    sv = _special_values(art.knots)
+    rng = np.random.default_rng(cfg * 100 + layer * 10 + bm * 2 + op)
+    for rows in (1, 31, 33, 1025, 2049):
+        X = rng.uniform(-1.6, 1.6, (rows, spec.in_dim)).astype(np.float32)
+        pos = rng.choice(X.size, size=min(X.size, 3 * sv.size), replace=False)
+        X.ravel()[pos] = np.resize(sv, pos.size)
+        _layer_parity(lk, oracle, art, X, f"C{cfg} l{layer} s{scheme} bm{bm} op{op} rows{rows}")
+
+
+def test_empty_and_single_row_everywhere(lk, oracle):
+    """rows = 0 and rows = 1 through every entry point (forward, chain, spline, eval, coords)."""
+    chain_o = [oracle.compile_layer(oracle.recipe_layer(2, l), 64, 0, 1, 0, 1, 0) for l in range(2)]
+    chain = [to_product_artifact(lk, a) for a in chain_o]
+    spec = lk.recipe_layer(2, 0)
+    for rows in (0, 1):
+        X = oracle.recipe_inputs(2, 0, max(rows, 1))[:rows]
+        Y, st = lk.lut_layer_forward_batch(chain[0], X)
+        assert Y.shape == (rows, 16) and st.n_samples == rows and st.n_inputs == rows * 78
+        r = lk.lut_model_forward_batch(chain, X)
+        assert r.Y.shape == (rows, 2) and len(r.per_layer) == 2
+        assert lk.layer_forward_batch(spec, X).shape == (rows, 16)
+        rep = lk.eval_accuracy(spec, chain[0], X)
+        assert rep.n_samples == rows
+        if rows:
+            Yo, sto = oracle.lut_model_forward(chain_o, X.astype(np.float64))
+            assert_close(r.Y, Yo, "single-row chain")
+            assert [stats_list(s) for s in r.per_layer] == sto.astype(int).tolist()
+
+
+def test_forward_c5_full_layer_row_subsample(lk, oracle):
+    """Maximum size: the whole C5 layer 0 (4096 x 4096 edges, K=16, L=128, uint8 asym, closed,
+    zero_spline: 68.7 GB of codes, stored tiles-only) compiled and evaluated on one GPU; 48 rows,
+    checked on column slices against the reference compiled on exactly those edges."""
+    spec = lk.recipe_layer(5, 0)
+    g = lk.compile_layer(spec, lk.QuantConfig(128, lk.Scheme.Asymmetric, lk.Dtype.Uint8),
+                         lk.OobConfig(lk.BoundaryMode.Closed, lk.OobPolicy.ZeroSpline))
+    X = lk.recipe_inputs(5, 0, 48)
+    Y, st = lk.lut_layer_forward_batch(g, X)
+    del g
+    for c0, c1 in ((0, 8), (2044, 2052), (4088, 4096)):
+        so = to_oracle_spec(lk.recipe_layer(5, 0, c0, c1))
+        ao = oracle.compile_layer(so, 128, 1, 1, 0, 1, 1)
+        Yo, sto = oracle.lut_forward(ao, X.astype(np.float64), nthreads=8)
+        assert_close(Y[:, c0:c1], Yo, f"C5 full layer cols {c0}:{c1}")
+        assert stats_list(st) == [int(v) for v in sto]  # OOB stats count inputs, not edges
