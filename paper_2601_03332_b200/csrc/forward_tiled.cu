@@ -39,6 +39,7 @@
 #include "coords.cuh"
 #include "lkg_internal.h"
 #include "tma.cuh"
+#include "tmem.cuh"
 
 namespace {
 
@@ -113,7 +114,17 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
     for (int s = 0; s < NS; s++) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // F64: the f64 accumulators live in Tensor Memory (tmem.cuh), not registers: each thread owns
+  // R x 16 doubles = R x 32 columns of its TMEM lane; warps w and w+4k share a lane quarter.
+  constexpr uint32_t kTmCols = F64 ? ((W / 4) * R * 32 <= 32 ? 32 : (W / 4) * R * 32 <= 64 ? 64
+                                      : (W / 4) * R * 32 <= 128 ? 128 : (W / 4) * R * 32 <= 256 ? 256 : 512) : 32;
+  uint32_t* tm_base_s = reinterpret_cast<uint32_t*>(full + 3);  // spare slot of the barrier block
+  if (F64 && warp == 0) lkg::tmem_alloc(tm_base_s, kTmCols);
+  if (F64) lkg::tmem_fence_before_sync();
   __syncthreads();
+  if (F64) lkg::tmem_fence_after_sync();
+  const uint32_t tm_base = F64 ? *tm_base_s : 0u;
+  const uint32_t tm_warp = tm_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * R * 32);
 
   const int64_t n_local = a.n_items > blockIdx.x ? (a.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t n_stages = n_local * a.n_ih;
@@ -193,16 +204,16 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
     const int64_t row0 = rt * (int64_t)(W * ROWS_W) + warp * ROWS_W;
     const int64_t rows_left = a.rows - row0;  // rows of this warp: [0, min(ROWS_W, rows_left))
     float2 acc[R][8];
-    double acc64[F64 ? R : 1][F64 ? 16 : 1];
     uint32_t row_oob = 0;   // bit r: row lane + 32 r saw an OOB coordinate
     uint32_t oob_item = 0;  // OOB coordinates of this lane's rows in this item
 #pragma unroll
     for (int r = 0; r < R; r++) {
 #pragma unroll
       for (int q = 0; q < 8; q++) acc[r][q] = make_float2(0.f, 0.f);
-      if (F64)
-#pragma unroll
-        for (int q = 0; q < 16; q++) acc64[r][q] = 0.0;
+      if (F64) {
+        const uint32_t zero[32] = {};
+        lkg::tmem_st32(tm_warp + 32 * r, zero);
+      }
     }
 
     for (int ih = 0; ih < a.n_ih; ih++, g++) {
@@ -313,14 +324,23 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
         }
       }
       if (F64 && ((ih + 1) % kFlushBlocks == 0 || ih + 1 == a.n_ih)) {
+        // fp32 tile partials into the f64 accumulators in TMEM (lo/hi word pairs)
 #pragma unroll
-        for (int r = 0; r < R; r++)
+        for (int r = 0; r < R; r++) {
+          uint32_t w[32];
+          lkg::tmem_ld32(tm_warp + 32 * r, w);
 #pragma unroll
           for (int q = 0; q < 8; q++) {
-            acc64[r][2 * q] += (double)acc[r][q].x;
-            acc64[r][2 * q + 1] += (double)acc[r][q].y;
+            const double d0 = __hiloint2double((int)w[4 * q + 1], (int)w[4 * q]) + (double)acc[r][q].x;
+            const double d1 = __hiloint2double((int)w[4 * q + 3], (int)w[4 * q + 2]) + (double)acc[r][q].y;
+            w[4 * q] = (uint32_t)__double2loint(d0);
+            w[4 * q + 1] = (uint32_t)__double2hiint(d0);
+            w[4 * q + 2] = (uint32_t)__double2loint(d1);
+            w[4 * q + 3] = (uint32_t)__double2hiint(d1);
             acc[r][q] = make_float2(0.f, 0.f);
           }
+          lkg::tmem_st32(tm_warp + 32 * r, w);
+        }
       }
       __syncthreads();  // every warp is done with this stage buffer
       if (tid == 0 && g + NS < n_stages) issue(g + NS);
@@ -331,13 +351,20 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
 #pragma unroll
     for (int r = 0; r < R; r++) {
       const int64_t row = row0 + lane + 32 * r;
-      if (lane + 32 * r < rows_left) {
-        float out[16];
+      float out[16];
+      if (F64) {  // warp-collective TMEM read: every lane, before the row bound
+        uint32_t w[32];
+        lkg::tmem_ld32(tm_warp + 32 * r, w);
+#pragma unroll
+        for (int q = 0; q < 16; q++) out[q] = (float)__hiloint2double((int)w[2 * q + 1], (int)w[2 * q]);
+      } else {
 #pragma unroll
         for (int q = 0; q < 8; q++) {
-          out[2 * q] = F64 ? (float)acc64[r][2 * q] : acc[r][q].x;
-          out[2 * q + 1] = F64 ? (float)acc64[r][2 * q + 1] : acc[r][q].y;
+          out[2 * q] = acc[r][q].x;
+          out[2 * q + 1] = acc[r][q].y;
         }
+      }
+      if (lane + 32 * r < rows_left) {
         if (FUSE) {
           // next layer (runtime.cpp:298-314 chain) on this row's hidden activations out[0..m)
           const int K2 = a.cc2.K, L2 = a.cc2.L, MP2 = a.MP2;
@@ -406,6 +433,12 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   }
   nonfinite |= !(nfacc == 0.0f);
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicExch(a.counters + 2, 1ull);
+  if (F64) {  // every warp is done with TMEM
+    lkg::tmem_fence_before_sync();
+    __syncthreads();
+    lkg::tmem_fence_after_sync();
+    if (warp == 0) lkg::tmem_dealloc(tm_base, kTmCols);
+  }
   if (FUSE) {
     unsigned long long oi2 = oob2_inputs, orow2 = oob2_rows;
     for (int o = 16; o; o >>= 1) {
@@ -647,7 +680,7 @@ void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
 namespace lkg {
 
 static constexpr int kW = 16, kR = 2;          // fp32 mode: 16 warps x 64 rows = 1024-row tiles
-static constexpr int kW64 = 16, kR64 = 1;      // f64-flush mode: 16 warps x 32 rows = 512-row tiles
+static constexpr int kW64 = 16, kR64 = 2;      // f64 mode: 16 warps x 64 rows, f64 accumulators in TMEM
 static constexpr int kSmallMaxBytes = 200 * 1024;
 
 bool tiled_eligible(const lkg_layer* L) {
