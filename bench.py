@@ -26,9 +26,16 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# stdout carries exactly one JSON line: keep NCCL's version banner (NCCL_DEBUG=VERSION) off it
-if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-    os.environ["NCCL_DEBUG"] = "WARN"
+# stdout carries exactly one JSON line: everything else written to fd 1 by native code (NCCL's
+# version banner, library diagnostics) is sent to stderr; the result line goes to the saved stdout.
+_RESULT_OUT = os.fdopen(os.dup(1), "w")
+os.dup2(2, 1)
+sys.stdout = sys.stderr
+
+
+def emit(line: dict) -> None:
+    _RESULT_OUT.write(json.dumps(line) + "\n")
+    _RESULT_OUT.flush()
 
 import numpy as np  # noqa: E402
 
@@ -132,7 +139,7 @@ def run_reference(args, wl):
                              "sample": f"{sample_rows} rows of {wl} per step (reference lut_model_forward_batch, "
                                        f"Tier::Optimized, rows sharded over {nthreads} threads)"},
             "e2e": {"value": value, "unit": "edge-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def ncu_traffic(key):
@@ -246,7 +253,7 @@ def run_c5(args):
                 "e2e": None, "gpu_launches": eng.launch_count - n0, "clocks": clk.summary(),
                 "compile": {"gpu_s": compile_s, "note": "host recipe generation + device compile, this rank"},
                 "oob_any_frac_layer0": st[0].oob_any_frac()}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -441,7 +448,7 @@ def main():
                 line["cpu_baseline"] = cpu_baseline(args.workload)
             except Exception as ex:  # the oracle is optional on the box; say why it is missing
                 line["cpu_baseline"] = {"value": None, "error": repr(ex)}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
