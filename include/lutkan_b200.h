@@ -214,6 +214,28 @@ lkg_status lkg_artifact_load(lkg_ctx* ctx, const char* path, lkg_layer** out);
 lkg_status lkg_artifact_save_desc(const lkg_layer_desc* desc, const char* path, int32_t mode);
 lkg_status lkg_artifact_check(const char* path);
 
+/* ---------------------------------------------- element primitives (§8a) */
+/* The reference's scalar functions, batched on the device in f64 with the reference's
+ * expressions (values identical to the reference's); HOST arrays of n elements, synchronous.
+ * safe_clip / segment_index / interp_coords / in_range (runtime.cpp:45-75) of x[n] against the
+ * layer's knots (any output may be NULL). */
+lkg_status lkg_lut_coords64(lkg_ctx* ctx, const lkg_layer* layer, const double* x, int64_t n, uint8_t* in_range,
+                            double* x_clip, int32_t* k, int32_t* l0, int32_t* l1, double* w);
+/* lut_eval_value / lut_eval_phi (runtime.cpp:96-120) of edges e[n] at x[n]: NON_FINITE for a
+ * non-finite x, DIMENSION for an edge out of range, UNSUPPORTED_BASE for an unknown base kind. */
+lkg_status lkg_lut_eval(lkg_ctx* ctx, const lkg_layer* layer, const int32_t* e, const double* x, int64_t n,
+                        double* value, uint8_t* was_oob, double* phi);
+/* basis_values (spline.cpp:89-94) over KnotGrid(breakpoints[K+1], degree): out [n][K+degree]. */
+lkg_status lkg_basis_values(lkg_ctx* ctx, const double* breakpoints, int32_t K, int32_t degree, const double* x,
+                            int64_t n, double* out);
+/* eval_edge_phi (spline.cpp:96-115) of the spec's edges e[n] at x[n]. */
+lkg_status lkg_edge_phi(lkg_ctx* ctx, const lkg_spec* spec, const int32_t* e, const double* x, int64_t n,
+                        double* phi);
+/* quantize_segment_symmetric / _asymmetric (compiler.cpp:105-128) of nseg segments of L values
+ * (v [nseg][L]): codes q [nseg][L], unrounded scale / y_min [nseg]. */
+lkg_status lkg_quantize_segments(lkg_ctx* ctx, const double* v, int64_t nseg, int32_t L, int32_t scheme, int32_t* q,
+                                 double* scale, double* y_min);
+
 /* ------------------------------------------- accuracy */
 /* eval_accuracy(layer, artifact, X) (metrics.cpp:30-103): |lut_eval_phi - eval_edge_phi| over
  * every (sample, input, edge), bucketed in-range / OOB / boundary; f64 on the device with the

@@ -97,6 +97,11 @@ SIGNATURES = {
     "lkg_artifact_load": (C.c_int, [C.c_void_p, C.c_char_p, _P(C.c_void_p)]),
     "lkg_artifact_save_desc": (C.c_int, [_P(LayerDesc), C.c_char_p, C.c_int32]),
     "lkg_artifact_check": (C.c_int, [C.c_char_p]),
+    "lkg_lut_coords64": (C.c_int, [C.c_void_p, C.c_void_p, f64p, C.c_int64, u8p, f64p, i32p, i32p, i32p, f64p]),
+    "lkg_lut_eval": (C.c_int, [C.c_void_p, C.c_void_p, i32p, f64p, C.c_int64, f64p, u8p, f64p]),
+    "lkg_basis_values": (C.c_int, [C.c_void_p, f64p, C.c_int32, C.c_int32, f64p, C.c_int64, f64p]),
+    "lkg_edge_phi": (C.c_int, [C.c_void_p, C.c_void_p, i32p, f64p, C.c_int64, f64p]),
+    "lkg_quantize_segments": (C.c_int, [C.c_void_p, f64p, C.c_int64, C.c_int32, C.c_int32, i32p, f64p, f64p]),
     "lkg_eval_accuracy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, _P(EvalReportC)]),
     "lkg_eval_accuracy_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                          _P(EvalReportC)]),

@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include")]
 # The compile kernel must not contract f64 multiply-adds (bit-exact LUT bytes).
-PER_FILE = {"compile.cu": ["-fmad=false"], "eval.cu": ["-fmad=false"]}
+PER_FILE = {"compile.cu": ["-fmad=false"], "eval.cu": ["-fmad=false"], "elements.cu": ["-fmad=false"]}
 
 
 def _newer(src: str, obj: str, headers: list[str]) -> bool:

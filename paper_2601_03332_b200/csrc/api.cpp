@@ -97,6 +97,16 @@ struct DeviceGuard {
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
+// KnotGrid validation (spline.cpp:8-27)
+void check_breakpoints(const std::vector<double>& bp, int degree) {
+  if (degree < 0) fail(LKG_ERR_CONFIG, "degree must be >= 0");
+  if (bp.size() < 2) fail(LKG_ERR_CONFIG, "need at least 2 breakpoints");
+  for (size_t i = 0; i < bp.size(); i++) {
+    if (!std::isfinite(bp[i])) fail(LKG_ERR_NON_FINITE, "non-finite breakpoint");
+    if (i > 0 && !(bp[i - 1] < bp[i])) fail(LKG_ERR_CONFIG, "breakpoints must be strictly increasing");
+  }
+}
+
 void check_knots(const float* knots, int K) {
   if (K < 1) fail(LKG_ERR_CONFIG, "artifact needs at least 2 knots");
   for (int i = 0; i <= K; i++) {
@@ -741,6 +751,182 @@ lkg_status lkg_spline_forward_host(lkg_ctx* ctx, const lkg_spec* S, const float*
     LKG_CUDA(cudaMemcpyAsync(dX, Xh, xb, cudaMemcpyHostToDevice, ctx->stream));
     lkg::launch_spline(ctx, S, dX, rows, dY, nullptr);
     LKG_CUDA(cudaMemcpyAsync(Yh, dY, yb, cudaMemcpyDeviceToHost, ctx->stream));
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// ---------------------------------------------------------------- element primitives
+// Host arrays in and out (these are per-element utilities; the copies are small next to a batch).
+extern "C++" {
+namespace {
+struct Staging {
+  lkg::DBuf buf;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t n) {  // 256-byte aligned slices of one device allocation
+    T* p = reinterpret_cast<T*>(buf.as<char>() + off);
+    off += (sizeof(T) * n + 255) / 256 * 256;
+    return p;
+  }
+};
+size_t slice(size_t bytes) { return (bytes + 255) / 256 * 256; }
+void h2d(void* d, const void* h, size_t b, cudaStream_t st) {
+  if (b) LKG_CUDA(cudaMemcpyAsync(d, h, b, cudaMemcpyHostToDevice, st));
+}
+void d2h(void* h, const void* d, size_t b, cudaStream_t st) {
+  if (h && b) LKG_CUDA(cudaMemcpyAsync(h, d, b, cudaMemcpyDeviceToHost, st));
+}
+}  // namespace
+}  // extern "C++"
+
+lkg_status lkg_lut_coords64(lkg_ctx* ctx, const lkg_layer* L, const double* x, int64_t n, uint8_t* in_range,
+                            double* x_clip, int32_t* k, int32_t* l0, int32_t* l1, double* w) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(L, "layer");
+    if (n < 0) fail(LKG_ERR_DIMENSION, "negative element count");
+    if (n == 0) return;
+    need(x, "x");
+    DeviceGuard g(ctx->device);
+    Staging s;
+    s.buf.alloc(slice(8 * n) * 3 + slice(n) + slice(4 * n) * 3);
+    double* dx = s.take<double>(n);
+    double* dxc = s.take<double>(n);
+    double* dw = s.take<double>(n);
+    uint8_t* din = s.take<uint8_t>(n);
+    int32_t* dk = s.take<int32_t>(n);
+    int32_t* dl0 = s.take<int32_t>(n);
+    int32_t* dl1 = s.take<int32_t>(n);
+    h2d(dx, x, 8 * n, ctx->stream);
+    lkg::launch_coords64(ctx, L, dx, n, din, dxc, dk, dl0, dl1, dw);
+    d2h(in_range, din, n, ctx->stream);
+    d2h(x_clip, dxc, 8 * n, ctx->stream);
+    d2h(k, dk, 4 * n, ctx->stream);
+    d2h(l0, dl0, 4 * n, ctx->stream);
+    d2h(l1, dl1, 4 * n, ctx->stream);
+    d2h(w, dw, 8 * n, ctx->stream);
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+lkg_status lkg_lut_eval(lkg_ctx* ctx, const lkg_layer* L, const int32_t* e, const double* x, int64_t n,
+                        double* value, uint8_t* was_oob, double* phi) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(L, "layer");
+    if (n < 0) fail(LKG_ERR_DIMENSION, "negative element count");
+    if (n == 0) return;
+    need(e, "e");
+    need(x, "x");
+    if (L->value_repr == LKG_REPR_SPLINE_COMPONENT && L->base_kind != "silu")  // base_fn, spline.cpp:105-108
+      fail(LKG_ERR_UNSUPPORTED_BASE, "unsupported base kind: \"" + L->base_kind + "\"");
+    DeviceGuard g(ctx->device);
+    Staging s;
+    s.buf.alloc(slice(8 * n) * 3 + slice(4 * n) + slice(n) + 256);
+    double* dx = s.take<double>(n);
+    double* dv = s.take<double>(n);
+    double* dp = s.take<double>(n);
+    int32_t* de = s.take<int32_t>(n);
+    uint8_t* doob = s.take<uint8_t>(n);
+    int* flags = s.take<int>(2);
+    LKG_CUDA(cudaMemsetAsync(flags, 0, 8, ctx->stream));
+    h2d(dx, x, 8 * n, ctx->stream);
+    h2d(de, e, 4 * n, ctx->stream);
+    lkg::launch_lut_eval(ctx, L, de, dx, n, dv, doob, dp, flags);
+    int hf[2];
+    d2h(hf, flags, 8, ctx->stream);
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hf[0]) fail(LKG_ERR_NON_FINITE, "non-finite input value");  // runtime.cpp:97 (checked first)
+    if (hf[1]) fail(LKG_ERR_DIMENSION, "edge index out of range");
+    d2h(value, dv, 8 * n, ctx->stream);
+    d2h(was_oob, doob, n, ctx->stream);
+    d2h(phi, dp, 8 * n, ctx->stream);
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+lkg_status lkg_basis_values(lkg_ctx* ctx, const double* bp, int32_t K, int32_t degree, const double* x, int64_t n,
+                            double* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(bp, "breakpoints");
+    if (n < 0) fail(LKG_ERR_DIMENSION, "negative element count");
+    if (K < 1) fail(LKG_ERR_CONFIG, "need at least 2 breakpoints");
+    std::vector<double> b(bp, bp + K + 1);
+    check_breakpoints(b, degree);
+    if (n == 0) return;
+    need(x, "x");
+    need(out, "out");
+    DeviceGuard g(ctx->device);
+    const int64_t R = K + degree;
+    Staging s;
+    s.buf.alloc(slice(8 * n) + slice(8 * n * R));
+    double* dx = s.take<double>(n);
+    double* dout = s.take<double>(n * R);
+    h2d(dx, x, 8 * n, ctx->stream);
+    lkg::launch_basis(ctx, b, degree, dx, n, dout);
+    d2h(out, dout, 8 * n * R, ctx->stream);
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+lkg_status lkg_edge_phi(lkg_ctx* ctx, const lkg_spec* S, const int32_t* e, const double* x, int64_t n, double* phi) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(S, "spec");
+    if (n < 0) fail(LKG_ERR_DIMENSION, "negative element count");
+    if (n == 0) return;
+    need(e, "e");
+    need(x, "x");
+    need(phi, "phi");
+    DeviceGuard g(ctx->device);
+    Staging s;
+    s.buf.alloc(slice(8 * n) * 2 + slice(4 * n) + 256);
+    double* dx = s.take<double>(n);
+    double* dp = s.take<double>(n);
+    int32_t* de = s.take<int32_t>(n);
+    int* flags = s.take<int>(2);
+    LKG_CUDA(cudaMemsetAsync(flags, 0, 8, ctx->stream));
+    h2d(dx, x, 8 * n, ctx->stream);
+    h2d(de, e, 4 * n, ctx->stream);
+    lkg::launch_edge_phi(ctx, S, de, dx, n, dp, flags);
+    int hf[2];
+    d2h(hf, flags, 8, ctx->stream);
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hf[1]) fail(LKG_ERR_DIMENSION, "edge index out of range");
+    d2h(phi, dp, 8 * n, ctx->stream);
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+lkg_status lkg_quantize_segments(lkg_ctx* ctx, const double* v, int64_t nseg, int32_t L, int32_t scheme, int32_t* q,
+                                 double* scale, double* y_min) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (nseg < 0) fail(LKG_ERR_DIMENSION, "negative segment count");
+    if (L < 1) fail(LKG_ERR_CONFIG, "cannot quantize an empty segment");  // compiler.cpp:80
+    if (scheme != LKG_SCHEME_SYMMETRIC && scheme != LKG_SCHEME_ASYMMETRIC) fail(LKG_ERR_CONFIG, "unknown scheme");
+    if (nseg == 0) return;
+    need(v, "values");
+    DeviceGuard g(ctx->device);
+    const int64_t n = nseg * L;
+    Staging s;
+    s.buf.alloc(slice(8 * n) + slice(4 * n) + slice(8 * nseg) * 2 + 256);
+    double* dv = s.take<double>(n);
+    int32_t* dq = s.take<int32_t>(n);
+    double* ds = s.take<double>(nseg);
+    double* dy = s.take<double>(nseg);
+    int* flags = s.take<int>(2);
+    LKG_CUDA(cudaMemsetAsync(flags, 0, 8, ctx->stream));
+    h2d(dv, v, 8 * n, ctx->stream);
+    lkg::launch_quantize(ctx, dv, nseg, L, scheme == LKG_SCHEME_ASYMMETRIC, dq, ds, dy, flags);
+    int hf[2];
+    d2h(hf, flags, 8, ctx->stream);
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hf[0]) fail(LKG_ERR_NON_FINITE, "non-finite table value");
+    d2h(q, dq, 4 * n, ctx->stream);
+    d2h(scale, ds, 8 * nseg, ctx->stream);
+    d2h(y_min, dy, 8 * nseg, ctx->stream);
     LKG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }

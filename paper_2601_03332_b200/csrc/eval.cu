@@ -21,14 +21,15 @@
 #include <cstdint>
 #include <vector>
 
+#include "f64ref.cuh"
 #include "lkg_internal.h"
 
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMaxP = 7;
-constexpr int kMaxT = 96;
-constexpr int kMaxK = 64;
+using lkg::f64ref::kMaxK;
+using lkg::f64ref::kMaxP;
+using lkg::f64ref::kMaxT;
 
 struct EvalArgs {
   const float* X;
@@ -49,13 +50,8 @@ struct EvalArgs {
   unsigned long long* u;       // [0,1] max bits (in, oob), [2..5] n_in, n_oob, n_boundary, n_oob_samples, [6] nonfinite
 };
 
-__device__ __forceinline__ double silu_d(double x) { return x / (1.0 + exp(-x)); }  // spline.cpp:85
-
 __device__ __forceinline__ double fetch(const EvalArgs& a, int64_t cell, int l) {  // runtime.cpp:81-88
-  const int64_t off = cell * a.L + l;
-  if (a.ftab) return a.ftab[off];
-  const double qv = a.i8 ? (double)(int8_t)a.q[off] : (double)a.q[off];
-  return (double)a.ymin[cell] + (double)a.scale[cell] * qv;
+  return lkg::f64ref::fetch(a.q, a.scale, a.ymin, a.ftab, a.i8, a.L, cell, l);
 }
 
 __global__ void __launch_bounds__(kThreads) eval_kernel(const __grid_constant__ EvalArgs a) {
@@ -67,7 +63,7 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const __grid_constant__ 
   const int r = t / a.JT, jt = t - r * a.JT;
   const int64_t row = (int64_t)blockIdx.x * a.RB + r;
   const int j = blockIdx.y * a.JT + jt;
-  const int p = a.p, n0 = a.nT - 1;
+  const int p = a.p;
   const int64_t E = (int64_t)a.d * a.m;
   double sum_in = 0.0, max_in = 0.0, sum_oob = 0.0, max_oob = 0.0;
   unsigned long long n_in = 0, n_oob = 0, n_bd = 0;
@@ -84,47 +80,21 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const __grid_constant__ 
       const bool interior = a.lo <= x && x < a.hi;
       fl = (in ? 1 : 0) | (interior ? 2 : 0);
       if (!in) s_rowoob[r] = 1;
-      // spline basis window (spline.cpp:69-83): b[o] = B_{mu-p+o}(x)
-      int mu = -1;
-      for (int s = 0; s < n0; s++)
-        if (a.T[s] <= x && x < a.T[s + 1]) mu = s;
+      // spline basis window (spline.cpp:69-83): b[o] = B_{r0+o}(x)
       double b[kMaxP + 1];
-      for (int o = 0; o <= kMaxP; o++) b[o] = 0.0;
-      if (mu >= 0) {
-        b[p] = 1.0;
-        for (int qq = 1; qq <= p; qq++) {
-          for (int o = p - qq; o <= p; o++) {
-            const int rr = mu - p + o;
-            if (rr < 0 || rr >= n0 - qq) {
-              b[o] = 0.0;
-              continue;
-            }
-            double acc = 0.0;
-            const double d1 = a.T[rr + qq] - a.T[rr];
-            if (d1 > 0.0) acc += (x - a.T[rr]) / d1 * b[o];
-            const double d2 = a.T[rr + qq + 1] - a.T[rr + 1];
-            if (d2 > 0.0 && o + 1 <= p) acc += (a.T[rr + qq + 1] - x) / d2 * b[o + 1];
-            b[o] = acc;
-          }
-        }
-      }
+      int r0;
+      lkg::f64ref::basis_window(a.T, a.nT, p, x, b, &r0);
       for (int o = 0; o <= kMaxP; o++) s_b[t][o] = b[o];
-      s_r0[t] = mu - p;
-      s_base[t] = silu_d(x);  // base_fn(silu, x) on the raw input (metrics.cpp:60)
+      s_r0[t] = r0;
+      s_base[t] = lkg::f64ref::silu(x);  // base_fn(silu, x) on the raw input (metrics.cpp:60)
       // table coordinates (runtime.cpp:45-69)
-      const double xp = x < a.lo ? a.lo : (x > a.hi_clip ? a.hi_clip : x);
-      int k = 0;
-      while (k + 1 <= a.K && a.kn[k + 1] <= xp) k++;  // upper_bound - 1
-      k = k > a.K - 1 ? a.K - 1 : k;
-      const double u = (xp - a.kn[k]) / (a.kn[k + 1] - a.kn[k]);
-      const double z = u * (double)(a.L - 1);
-      int l0 = (int)floor(z);
-      l0 = l0 < 0 ? 0 : (l0 > a.L - 1 ? a.L - 1 : l0);
-      s_k[t] = k;
-      s_l0[t] = l0;
-      s_l1[t] = l0 + 1 < a.L - 1 ? l0 + 1 : a.L - 1;
-      s_w[t] = z - (double)l0;
-      s_bxl[t] = a.phi ? 0.0 : silu_d(a.zs ? x : xp);  // runtime.cpp:113-115
+      const lkg::f64ref::Coord64 c = lkg::f64ref::coords(a.kn, a.K, a.L, a.half_open, a.hi_clip, x);
+      const double xp = c.xp;
+      s_k[t] = c.k;
+      s_l0[t] = c.l0;
+      s_l1[t] = c.l1;
+      s_w[t] = c.w;
+      s_bxl[t] = a.phi ? 0.0 : lkg::f64ref::silu(a.zs ? x : xp);  // runtime.cpp:113-115
       s_fl[t] = fl;
     }
     __syncthreads();

@@ -143,7 +143,17 @@ void launch_fuse_gains(lkg_ctx* ctx, lkg_layer* L);
 void launch_coords(lkg_ctx* ctx, const lkg_layer* L, const float* x, int64_t n, int32_t* in_range, int32_t* k,
                    int32_t* l0);
 void launch_spec_prepare(lkg_ctx* ctx, lkg_spec* S);
-void validate_layer_desc(const lkg_layer_desc* d);  // finalize checks (runtime.cpp:11-43)
+void validate_layer_desc(const lkg_layer_desc* d);
+// element primitives (elements.cu), device pointers
+void launch_coords64(lkg_ctx* ctx, const lkg_layer* L, const double* x, int64_t n, uint8_t* in, double* xc,
+                     int32_t* k, int32_t* l0, int32_t* l1, double* w);
+void launch_lut_eval(lkg_ctx* ctx, const lkg_layer* L, const int32_t* e, const double* x, int64_t n, double* value,
+                     uint8_t* was_oob, double* phi, int* flags);
+void launch_basis(lkg_ctx* ctx, const std::vector<double>& bp, int degree, const double* x, int64_t n, double* out);
+void launch_edge_phi(lkg_ctx* ctx, const lkg_spec* S, const int32_t* e, const double* x, int64_t n, double* phi,
+                     int* flags);
+void launch_quantize(lkg_ctx* ctx, const double* v, int64_t nseg, int L, int asym, int32_t* q, double* scale,
+                     double* ymin, int* flags);  // finalize checks (runtime.cpp:11-43)
 void launch_eval(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const float* X, int64_t rows,
                  double* dsum, unsigned long long* u);
 bool launch_spline_tiled(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows, float* Y);

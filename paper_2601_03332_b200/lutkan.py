@@ -619,6 +619,152 @@ def layer_forward_batch(layer: KanLayerSpec, X, tier: Tier = Tier.Optimized, eng
     return Y
 
 
+# ------------------------------------------------------------------ element primitives (§8a F7-F13, S2, CM3-CM9)
+def _f64(x):
+    return np.ascontiguousarray(np.atleast_1d(np.asarray(x, np.float64)))
+
+
+def lut_coords(a: "LutLayerArtifact", x, engine: Engine | None = None) -> dict:
+    """safe_clip / segment_index / interp_coords / in_range (runtime.cpp:45-75) of every x, on the
+    device in f64: dict of in_range, x_clip, k, l0, l1, w arrays."""
+    eng = engine or default_engine()
+    xv = _f64(x)
+    n = xv.size
+    out = dict(in_range=np.zeros(n, np.uint8), x_clip=np.zeros(n), k=np.zeros(n, np.int32),
+               l0=np.zeros(n, np.int32), l1=np.zeros(n, np.int32), w=np.zeros(n))
+    check(lib().lkg_lut_coords64(eng.handle, a.device(eng).handle, xv.ctypes.data_as(_capi.f64p), n,
+                                 *[out[k].ctypes.data_as(t) for k, t in (("in_range", _capi.u8p), ("x_clip", _capi.f64p),
+                                                                         ("k", _capi.i32p), ("l0", _capi.i32p),
+                                                                         ("l1", _capi.i32p), ("w", _capi.f64p))]))
+    out["in_range"] = out["in_range"].astype(bool)
+    return out
+
+
+def in_range(a: "LutLayerArtifact", x, engine: Engine | None = None):
+    """runtime.cpp:71-75."""
+    r = lut_coords(a, x, engine)["in_range"]
+    return bool(r[0]) if np.isscalar(x) else r
+
+
+def _lut_eval(a, e, x, engine):
+    eng = engine or default_engine()
+    xv, ev = _f64(x), np.ascontiguousarray(np.atleast_1d(np.asarray(e, np.int32)))
+    ev, xv = np.broadcast_arrays(ev, xv)
+    ev, xv = np.ascontiguousarray(ev, np.int32), np.ascontiguousarray(xv, np.float64)
+    n = xv.size
+    val, oob, phi = np.zeros(n), np.zeros(n, np.uint8), np.zeros(n)
+    check(lib().lkg_lut_eval(eng.handle, a.device(eng).handle, ev.ctypes.data_as(_capi.i32p),
+                             xv.ctypes.data_as(_capi.f64p), n, val.ctypes.data_as(_capi.f64p),
+                             oob.ctypes.data_as(_capi.u8p), phi.ctypes.data_as(_capi.f64p)))
+    return val, oob.astype(bool), phi
+
+
+def lut_eval_value(a: "LutLayerArtifact", e, x, engine: Engine | None = None):
+    """runtime.cpp:96-109: (value, was_oob) of edge e at x (scalars or broadcastable arrays)."""
+    v, o, _ = _lut_eval(a, e, x, engine)
+    return (float(v[0]), bool(o[0])) if np.isscalar(x) and np.isscalar(e) else (v, o)
+
+
+def lut_eval_phi(a: "LutLayerArtifact", e, x, engine: Engine | None = None):
+    """runtime.cpp:111-120."""
+    _, _, p = _lut_eval(a, e, x, engine)
+    return float(p[0]) if np.isscalar(x) and np.isscalar(e) else p
+
+
+def basis_values(grid: KnotGrid, x, engine: Engine | None = None):
+    """spline.cpp:89-94: the R = K + degree basis values at x ([R], or [n, R] for an array x)."""
+    eng = engine or default_engine()
+    xv = _f64(x)
+    bp = np.ascontiguousarray(grid.breakpoints, np.float64)
+    R = grid.K + grid.degree
+    out = np.zeros((xv.size, R))
+    check(lib().lkg_basis_values(eng.handle, bp.ctypes.data_as(_capi.f64p), grid.K, grid.degree,
+                                 xv.ctypes.data_as(_capi.f64p), xv.size, out.ctypes.data_as(_capi.f64p)))
+    return out[0] if np.isscalar(x) else out
+
+
+def eval_spline(grid: KnotGrid, coeffs, x, engine: Engine | None = None):
+    """spline.cpp:96-103: sum_r c_r B_r(x), r ascending (the reference's order, element-wise)."""
+    c = np.asarray(coeffs, np.float64)
+    if c.size != grid.K + grid.degree:
+        raise DimensionError("coefficient count does not match basis count")
+    b = np.atleast_2d(basis_values(grid, x, engine))
+    acc = np.zeros(b.shape[0])
+    for r in range(c.size):
+        acc = acc + c[r] * b[:, r]
+    return float(acc[0]) if np.isscalar(x) else acc
+
+
+def base_fn(kind: str, x):
+    """spline.cpp:105-108."""
+    if kind != "silu":
+        raise UnsupportedBaseError(f'unsupported base kind: "{kind}"')
+    xv = np.asarray(x, np.float64)
+    return xv / (1.0 + np.exp(-xv))
+
+
+def eval_edge_phi(layer: KanLayerSpec, e, x, engine: Engine | None = None):
+    """spline.cpp:110-115 for edge e = i*out_dim + j of the layer, on the device in f64."""
+    if layer.base_kind != "silu":
+        raise UnsupportedBaseError(f'unsupported base kind: "{layer.base_kind}"')
+    eng = engine or default_engine()
+    xv, ev = _f64(x), np.ascontiguousarray(np.atleast_1d(np.asarray(e, np.int32)))
+    ev, xv = np.broadcast_arrays(ev, xv)
+    ev, xv = np.ascontiguousarray(ev, np.int32), np.ascontiguousarray(xv, np.float64)
+    phi = np.zeros(xv.size)
+    check(lib().lkg_edge_phi(eng.handle, layer.device(eng).handle, ev.ctypes.data_as(_capi.i32p),
+                             xv.ctypes.data_as(_capi.f64p), xv.size, phi.ctypes.data_as(_capi.f64p)))
+    return float(phi[0]) if np.isscalar(x) and np.isscalar(e) else phi
+
+
+def layer_forward(layer: KanLayerSpec, x, tier: Tier = Tier.Optimized, engine: Engine | None = None):
+    """spline.cpp:117-125: one row."""
+    x = np.asarray(x, np.float32)
+    if x.ndim != 1 or x.size != layer.in_dim:
+        raise DimensionError("input size does not match in_dim")
+    return layer_forward_batch(layer, x[None, :], tier, engine)[0]
+
+
+def sample_segment_points(breakpoints, k: int, L: int) -> np.ndarray:
+    """compiler.cpp:18-27 (x = t_k + l*step, step = (t_k+1 - t_k)/L, right endpoint excluded)."""
+    bp = np.asarray(breakpoints, np.float64)
+    if L < 2:
+        raise ConfigError("samples_per_segment must be >= 2")
+    if k < 0 or k + 1 >= bp.size:
+        raise DimensionError("segment index out of range")
+    step = (bp[k + 1] - bp[k]) / float(L)
+    return bp[k] + np.arange(L, dtype=np.float64) * step
+
+
+def _quantize(values, scheme: int, engine):
+    eng = engine or default_engine()
+    v = np.ascontiguousarray(np.asarray(values, np.float64))
+    if v.size == 0:
+        raise ConfigError("cannot quantize an empty segment")
+    q, sc, ym = np.zeros(v.size, np.int32), np.zeros(1), np.zeros(1)
+    check(lib().lkg_quantize_segments(eng.handle, v.ctypes.data_as(_capi.f64p), 1, v.size, scheme,
+                                      q.ctypes.data_as(_capi.i32p), sc.ctypes.data_as(_capi.f64p),
+                                      ym.ctypes.data_as(_capi.f64p)))
+    return q, float(sc[0]), float(ym[0])
+
+
+def quantize_segment_symmetric(values, engine: Engine | None = None):
+    """compiler.cpp:105-114: (codes, scale, y_min) with scale = amax/127, y_min = 0."""
+    return _quantize(values, int(Scheme.Symmetric), engine)
+
+
+def quantize_segment_asymmetric(values, engine: Engine | None = None):
+    """compiler.cpp:116-128: (codes, scale, y_min) with y_min = min, scale = (max - min)/255."""
+    return _quantize(values, int(Scheme.Asymmetric), engine)
+
+
+def build_float_lut(layer: KanLayerSpec, config: QuantConfig | None = None, engine: Engine | None = None):
+    """compiler.cpp:29-73: the unquantized table values [E, K*L] (f64), as compile_layer_debug_float
+    produces them on the device."""
+    a = compile_layer_debug_float(layer, config, OobConfig(), engine)
+    return np.asarray(a.float_table).reshape(layer.in_dim * layer.out_dim, -1)
+
+
 # ------------------------------------------------------------------ artifact container (artifact_io.hpp)
 def save_artifact(artifact: "LutLayerArtifact", path, engine: Engine | None = None, store: bool = False,
                   parallel: bool = False) -> None:

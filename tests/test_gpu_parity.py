@@ -497,3 +497,88 @@ def test_forward_c5_full_layer_row_subsample(lk, oracle):
         Yo, sto = oracle.lut_forward(ao, X.astype(np.float64), nthreads=8)
         assert_close(Y[:, c0:c1], Yo, f"C5 full layer cols {c0}:{c1}")
         assert stats_list(st) == [int(v) for v in sto]  # OOB stats count inputs, not edges
+
+
+# ------------------------------------------------------------------ element primitives (§8a)
+def _adversarial_x(knots, L, rng, n=3000):
+    k64 = np.asarray(knots, np.float64)
+    nodes = (k64[:-1, None] + np.arange(L)[None, :] / (L - 1) * np.diff(k64)[:, None]).ravel()
+    xs = [k64, nodes, np.nextafter(k64, np.inf), np.nextafter(k64, -np.inf),
+          np.nextafter(nodes, np.inf), np.nextafter(nodes, -np.inf),
+          rng.uniform(k64[0] - 1, k64[-1] + 1, n), [0.0, -0.0, 1e300, -1e300, 5e-324]]
+    return np.concatenate([np.asarray(v, np.float64) for v in xs])
+
+
+@pytest.mark.parametrize("bm,op,scheme,vr", [(0, 0, 0, 1), (1, 1, 1, 1), (1, 0, 1, 0), (0, 1, 0, 0)])
+def test_element_primitives_lut(lk, oracle, bm, op, scheme, vr):
+    """lut_coords (safe_clip / segment_index / interp_coords / in_range), lut_eval_value and
+    lut_eval_phi on the device equal the reference's scalar functions (f64 inputs, including
+    every sample node and knot ±1 ulp): coordinates and values bit-exact, phi to exp() ulps."""
+    ao = oracle.compile_layer(oracle.recipe_layer(1, 0), 16, scheme, vr, 0, bm, op)
+    a = to_product_artifact(lk, ao)
+    rng = np.random.default_rng(bm * 4 + op)
+    x = _adversarial_x(ao.knots, 16, rng)
+    c = lk.lut_coords(a, x)
+    co = oracle.coords(ao, x)
+    for key in ("in_range", "x_clip", "k", "l0", "l1", "w"):
+        assert np.array_equal(c[key], co[key]), key
+    E = ao.in_dim * ao.out_dim
+    e = rng.integers(0, E, x.size).astype(np.int32)
+    v, oob = lk.lut_eval_value(a, e, x)
+    phi = lk.lut_eval_phi(a, e, x)
+    for t in range(0, x.size, 7):
+        vo, oo = oracle.eval_value(ao, int(e[t]), float(x[t]))
+        assert v[t] == vo and oob[t] == oo, t
+        po = oracle.eval_phi(ao, int(e[t]), float(x[t]))
+        assert abs(phi[t] - po) <= 4e-16 * max(1.0, abs(po)), (t, phi[t], po)
+    with pytest.raises(lk.NonFiniteError):
+        lk.lut_eval_phi(a, 0, np.nan)
+    with pytest.raises(lk.DimensionError):
+        lk.lut_eval_value(a, E, 0.5)
+
+
+def test_element_primitives_spline_and_quantize(lk, oracle):
+    """basis_values, eval_spline, eval_edge_phi, sample_segment_points and
+    quantize_segment_symmetric / _asymmetric on the device equal the reference's."""
+    rng = np.random.default_rng(9)
+    spec = lk.recipe_layer(3, 0)
+    so = to_oracle_spec(spec)
+    for bp, deg in ((spec.grid.breakpoints, 3), (np.cumsum(rng.uniform(0.1, 1, 7)) - 2, 2),
+                    (np.cumsum(rng.uniform(0.1, 1, 5)) - 1, 5)):
+        grid = lk.KnotGrid(np.asarray(bp, np.float64), deg)
+        x = _adversarial_x(bp, 8, rng, 500)
+        B = lk.basis_values(grid, x)
+        for t in range(0, x.size, 5):
+            assert np.array_equal(B[t], oracle.basis_values(bp, deg, float(x[t]))), t
+    x = _adversarial_x(spec.grid.breakpoints, 8, rng, 2000)
+    E = spec.in_dim * spec.out_dim
+    e = rng.integers(0, E, x.size).astype(np.int32)
+    phi = lk.eval_edge_phi(spec, e, x)
+    R = spec.grid.K + spec.grid.degree
+    coeffs = np.asarray(so.coeffs, np.float64).reshape(E, R)
+    for t in range(0, x.size, 11):
+        b = oracle.basis_values(spec.grid.breakpoints, 3, float(x[t]))
+        sp = 0.0
+        for r in range(R):
+            sp += float(coeffs[e[t], r]) * b[r]
+        ref = so.out_scale[e[t]] * (so.base_scale[e[t]] * (x[t] / (1.0 + np.exp(-x[t]))) + so.spline_scale[e[t]] * sp)
+        assert abs(phi[t] - ref) <= 4e-16 * max(1.0, abs(ref)), (t, phi[t], ref)
+        assert lk.eval_spline(spec.grid, spec.coeffs[e[t]], float(x[t])) == sp
+    for k in range(spec.grid.K):
+        pts = lk.sample_segment_points(spec.grid.breakpoints, k, 64)
+        step = (spec.grid.breakpoints[k + 1] - spec.grid.breakpoints[k]) / 64.0
+        assert np.array_equal(pts, [spec.grid.breakpoints[k] + l * step for l in range(64)])
+    for trial in range(40):
+        vals = rng.normal(0, rng.uniform(1e-3, 2), int(rng.integers(2, 130)))
+        if trial % 5 == 0:
+            vals[:] = vals[0]                      # degenerate (constant) segment
+        if trial % 7 == 0:
+            vals[::3] = -vals[0]                   # ties of |v| with opposite signs (amax / min / max)
+        for scheme, fn in ((0, lk.quantize_segment_symmetric), (1, lk.quantize_segment_asymmetric)):
+            q, s, y = fn(vals)
+            qo, so_, yo = oracle.quantize_segment(vals, scheme)
+            assert np.array_equal(q, qo) and s == so_ and y == yo, (trial, scheme)
+    with pytest.raises(lk.NonFiniteError):
+        lk.quantize_segment_symmetric([1.0, np.inf])
+    with pytest.raises(lk.ConfigError):
+        lk.quantize_segment_asymmetric([])
