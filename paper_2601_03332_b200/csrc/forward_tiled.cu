@@ -680,7 +680,7 @@ void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
 namespace lkg {
 
 static constexpr int kW = 16, kR = 2;          // fp32 mode: 16 warps x 64 rows = 1024-row tiles
-static constexpr int kW64 = 16, kR64 = 2;      // f64 mode: 16 warps x 64 rows, f64 accumulators in TMEM
+static constexpr int kW64 = kW, kR64 = kR;      // f64 mode: same shape, f64 accumulators in TMEM
 static constexpr int kSmallMaxBytes = 200 * 1024;
 
 bool tiled_eligible(const lkg_layer* L) {
@@ -976,7 +976,6 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   const int grid = (int)std::min<int64_t>(a.n_items, sm_count(ctx->device));
   size_t smem = tiled_smem(L, W, R);
   const int sel = (asym << 2) | (sr << 1) | (int)zs;
-  static const char* exp_cfg = getenv("LKG_TILED_CFG");  // tuning experiments (sym, spline_component, clip_x)
   if (gm.codes_global) {
     switch (sel) {
 #define CASE(S)                                                                                                \
@@ -989,21 +988,6 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
       CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
     }
-    LKG_CUDA(cudaGetLastError());
-    ctx->launches++;
-    return;
-  }
-  if (exp_cfg && !L2 && !f64 && sel == 2) {
-    int ew = 16, er = 2, eb = 1;
-    sscanf(exp_cfg, "%d,%d,%d", &ew, &er, &eb);
-    a.n_items = ((rows + (int64_t)ew * 32 * er - 1) / ((int64_t)ew * 32 * er)) * gm.n_jb;
-    const int g2 = (int)std::min<int64_t>(a.n_items, (int64_t)eb * sm_count(ctx->device));
-    const size_t sm2 = tiled_smem(L, ew, er);
-    if (ew == 16 && er == 1 && eb == 2) launch_tiled<1, 16, false, true, false, false, false, 2>(ctx->stream, a, sm2, g2);
-    else if (ew == 12 && er == 2) launch_tiled<2, 12, false, true, false, false, false, 1>(ctx->stream, a, sm2, g2);
-    else if (ew == 32 && er == 1) launch_tiled<1, 32, false, true, false, false, false, 1>(ctx->stream, a, sm2, g2);
-    else if (ew == 8 && er == 2 && eb == 2) launch_tiled<2, 8, false, true, false, false, false, 2>(ctx->stream, a, sm2, g2);
-    else throw Error{LKG_ERR_INVALID_ARG, "unknown LKG_TILED_CFG"};
     LKG_CUDA(cudaGetLastError());
     ctx->launches++;
     return;
