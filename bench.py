@@ -26,16 +26,22 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# stdout carries exactly one JSON line: everything else written to fd 1 by native code (NCCL's
-# version banner, library diagnostics) is sent to stderr; the result line goes to the saved stdout.
-_RESULT_OUT = os.fdopen(os.dup(1), "w")
-os.dup2(2, 1)
-sys.stdout = sys.stderr
+_RESULT_OUT = None
+
+
+def isolate_stdout() -> None:
+    """stdout carries exactly one JSON line: everything else written to fd 1 by native code (NCCL's
+    version banner, library diagnostics) goes to stderr; the result line to the saved stdout."""
+    global _RESULT_OUT
+    _RESULT_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    sys.stdout = sys.stderr
 
 
 def emit(line: dict) -> None:
-    _RESULT_OUT.write(json.dumps(line) + "\n")
-    _RESULT_OUT.flush()
+    out = _RESULT_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 import numpy as np  # noqa: E402
 
@@ -455,4 +461,5 @@ def main():
 
 
 if __name__ == "__main__":
+    isolate_stdout()
     main()
