@@ -87,7 +87,7 @@ int ork_eval_value(const ork_artifact* a, int32_t e, double x, double* value, in
 int ork_eval_phi(const ork_artifact* a, int32_t e, double x, double* value);
 
 /* Artifact container (artifact_io.cpp:206-300). REFERENCE LIBRARY ONLY: the port returns 99
- * (its pin is tests/golden/*.lut, written by the reference). Status codes 9..15 follow the
+ * (its pin is the .lut fixtures under tests/golden/artifacts, written by the reference). Status codes 9..15 follow the
  * IoError family as numbered in include/lutkan_b200.h. load_resave loads path and, when
  * resave_path != NULL, saves the loaded artifact again (a byte-level round trip). */
 int ork_artifact_save(const ork_artifact* a, const char* path);

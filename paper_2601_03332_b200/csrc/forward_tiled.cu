@@ -27,7 +27,11 @@
 //  * Zero_spline masking is folded into the P/Q offset: an out-of-bounds input reads the zero
 //    block, so its table term vanishes while the base branch stays live (runtime.cpp:183-189).
 //  * Accumulation: fp32 per lane; for long reductions (d > kFp32MaxD) the fp32 partial is
-//    flushed into an f64 accumulator every 64 inputs.
+//    flushed after every tile (8 inputs) into f64 accumulators held in Tensor Memory (tmem.cuh;
+//    SURVEY Appendix B.4).
+//  * Coordinates: lut_coords_fast (coords.cuh) for both rows side by side, the exact path once
+//    per step for any coordinate next to a sample node; x blocks arrive by cp.async one tile
+//    ahead; items are grouped (item_coords) so x blocks and tiles are reused in L2.
 #include <cuda_runtime.h>
 
 #include <cmath>
