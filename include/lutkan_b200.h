@@ -274,6 +274,13 @@ lkg_status lkg_recipe_dims(int32_t cfg, int32_t* n_layers, int32_t* dims_out, in
 lkg_status lkg_recipe_layer(int32_t cfg, int32_t layer, int32_t col0, int32_t col1,
                             double* breakpoints, double* coeffs, double* base_scale,
                             double* spline_scale, double* out_scale);
+/* gen_layer / gen_inputs (model_gen.cpp:7-45): the reference's generator (breakpoints on [-1, 1],
+ * coefficients normal(0, 0.1), gains uniform(0.5, 1.5); inputs standard normal, optionally
+ * clamped). Host functions; arrays [K+1], [E*(K+degree)], [E] x3, X [n*dim] f64. */
+lkg_status lkg_gen_layer(uint64_t seed, int32_t in_dim, int32_t out_dim, int32_t segments, int32_t degree,
+                         double* breakpoints, double* coeffs, double* base_scale, double* spline_scale,
+                         double* out_scale);
+lkg_status lkg_gen_inputs(uint64_t seed, int64_t n, int64_t dim, double lo, double hi, int32_t clip, double* X);
 /* fp32 inputs rows [row0, row0+rows). */
 lkg_status lkg_recipe_inputs(int32_t cfg, int64_t row0, int64_t rows, float* X);
 

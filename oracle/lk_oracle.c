@@ -775,6 +775,36 @@ int ork_recipe_layer(int32_t cfg, int32_t layer, double* bp, double* coeffs, dou
   return OK;
 }
 
+/* gen_layer (model_gen.cpp:7-27) */
+int ork_gen_layer(uint64_t seed, int32_t d, int32_t m, int32_t segments, int32_t degree, double* bp, double* coeffs,
+                  double* bs, double* ss, double* os) {
+  if (segments < 1) return fail(CONFIG, "segments must be >= 1");
+  for (int k = 0; k <= segments; k++) bp[k] = -1.0 + 2.0 * (double)k / segments;
+  rng_t r;
+  rng_init(&r, seed);
+  int R = segments + degree;
+  for (int64_t e = 0; e < (int64_t)d * m; e++) {
+    for (int q = 0; q < R; q++) coeffs[e * R + q] = rng_normal_ms(&r, 0.0, 0.1);
+    bs[e] = rng_uniform_ab(&r, 0.5, 1.5);
+    ss[e] = rng_uniform_ab(&r, 0.5, 1.5);
+    os[e] = rng_uniform_ab(&r, 0.5, 1.5);
+  }
+  return OK;
+}
+
+/* gen_inputs (model_gen.cpp:33-45) */
+int ork_gen_inputs(uint64_t seed, int64_t n, int64_t dim, double lo, double hi, int32_t clip, double* X) {
+  if (!(lo < hi)) return fail(CONFIG, "input range must satisfy lo < hi");
+  rng_t r;
+  rng_init(&r, seed);
+  for (int64_t t = 0; t < n * dim; t++) {
+    double x = rng_normal(&r);
+    if (clip) x = x < lo ? lo : (hi < x ? hi : x);
+    X[t] = x;
+  }
+  return OK;
+}
+
 int ork_recipe_inputs(int32_t cfg, int64_t row0, int64_t rows, float* X) {
   recipe_t r;
   int st = recipe_of(cfg, &r);

@@ -117,6 +117,12 @@ float ork_f16_bits_to_f32(uint16_t h);
 void ork_rng_uniform(uint64_t seed, int64_t n, double* out);
 void ork_rng_normal(uint64_t seed, int64_t n, double* out);
 
+/* gen_layer / gen_inputs (model_gen.cpp:7-45). Outputs caller-allocated: breakpoints [K+1],
+ * coeffs [E*(K+degree)], gains [E] x3; X [n*dim]. */
+int ork_gen_layer(uint64_t seed, int32_t in_dim, int32_t out_dim, int32_t segments, int32_t degree, double* bp,
+                  double* coeffs, double* base_scale, double* spline_scale, double* out_scale);
+int ork_gen_inputs(uint64_t seed, int64_t n, int64_t dim, double lo, double hi, int32_t clip, double* X);
+
 /* Synthetic BASELINE configs (SURVEY.md §8d recipe, pinned in DESIGN.md §3).
  * cfg: 1..5. Layer l of the chain for cfg; seed stream continues across layers, so
  * generation always walks layers 0..l. Outputs are caller-allocated [E*R] / [E]. */

@@ -148,6 +148,9 @@ class Oracle:
                                             _f64p, _u64p]
         L.ork_spline_forward.argtypes = [_P(_Spec), _f64p, C.c_int64, C.c_int32, C.c_int32, _f64p]
         L.ork_coords.argtypes = [_P(_Art), _f64p, C.c_int64, _u8p, _f64p, _i32p, _i32p, _i32p, _f64p]
+        L.ork_gen_layer.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _f64p, _f64p, _f64p,
+                                    _f64p, _f64p]
+        L.ork_gen_inputs.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, _f64p]
         L.ork_artifact_save.argtypes = [_P(_Art), C.c_char_p]
         L.ork_artifact_load_resave.argtypes = [C.c_char_p, C.c_char_p]
         L.ork_eval_accuracy.argtypes = [_P(_Spec), _P(_Art), _f64p, C.c_int64, C.c_int32, _f64p, _u64p, _i32p]
@@ -215,6 +218,18 @@ class Oracle:
         self._chk(self.lib.ork_spline_forward(C.byref(cs), _ptr(X, _f64p), X.shape[0], tier, nthreads,
                                               _ptr(Y, _f64p)))
         return Y
+
+    def gen_layer(self, seed, d, m, segments, degree=3):
+        """gen_layer (model_gen.cpp:7-27) -> Spec."""
+        R, E = segments + degree, d * m
+        bp, co, bs, ss, os_ = np.zeros(segments + 1), np.zeros(E * R), np.zeros(E), np.zeros(E), np.zeros(E)
+        self._chk(self.lib.ork_gen_layer(seed, d, m, segments, degree, *[_ptr(a, _f64p) for a in (bp, co, bs, ss, os_)]))
+        return Spec(d, m, bp, co, bs, ss, os_, degree)
+
+    def gen_inputs(self, seed, n, dim, lo, hi, clip):
+        X = np.zeros((n, dim))
+        self._chk(self.lib.ork_gen_inputs(seed, n, dim, lo, hi, int(clip), _ptr(X, _f64p)))
+        return X
 
     def artifact_save(self, a: Artifact, path) -> None:
         """save_artifact (artifact_io.cpp:206-219); reference library only."""

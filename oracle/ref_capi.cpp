@@ -16,6 +16,7 @@
 #include "lutkan/compiler.hpp"
 #include "lutkan/float16.hpp"
 #include "lutkan/metrics.hpp"
+#include "lutkan/model_gen.hpp"
 #include "lutkan/rng.hpp"
 #include "lutkan/runtime.hpp"
 #include "lutkan/spline.hpp"
@@ -241,6 +242,27 @@ int ork_spline_forward(const ork_spec* s, const double* X, int64_t rows, int32_t
       Matrix Ys = layer_forward_batch(spec, Xs, t);  // spline.cpp:183-187
       std::memcpy(Y + r0 * s->out_dim, Ys.data.data(), sizeof(double) * Ys.data.size());
     });
+  });
+}
+
+int ork_gen_layer(uint64_t seed, int32_t d, int32_t m, int32_t segments, int32_t degree, double* bp, double* coeffs,
+                  double* bs, double* ss, double* os) {
+  return guarded([&] {
+    const KanLayerSpec s = gen_layer(seed, d, m, segments, degree);  // model_gen.cpp:7-27
+    const auto& b = s.grid().breakpoints();
+    std::copy(b.begin(), b.end(), bp);
+    const auto& c = s.packed_coeffs();
+    std::copy(c.begin(), c.end(), coeffs);
+    std::copy(s.base_scales().begin(), s.base_scales().end(), bs);
+    std::copy(s.spline_scales().begin(), s.spline_scales().end(), ss);
+    std::copy(s.out_scales().begin(), s.out_scales().end(), os);
+  });
+}
+
+int ork_gen_inputs(uint64_t seed, int64_t n, int64_t dim, double lo, double hi, int32_t clip, double* X) {
+  return guarded([&] {
+    const Matrix M = gen_inputs(seed, static_cast<std::size_t>(n), static_cast<std::size_t>(dim), lo, hi, clip != 0);
+    std::copy(M.data.begin(), M.data.end(), X);
   });
 }
 

@@ -111,6 +111,9 @@ SIGNATURES = {
                                             C.c_void_p, _P(OobStatsC)]),
     "lkg_recipe_dims": (C.c_int, [C.c_int32, i32p, i32p, i32p, f64p, f64p]),
     "lkg_recipe_layer": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, f64p, f64p, f64p, f64p, f64p]),
+    "lkg_gen_layer": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, f64p, f64p, f64p, f64p,
+                                f64p]),
+    "lkg_gen_inputs": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, C.c_double, C.c_double, C.c_int32, f64p]),
     "lkg_recipe_inputs": (C.c_int, [C.c_int32, C.c_int64, C.c_int64, f32p]),
 }
 

@@ -1108,6 +1108,30 @@ lkg_status lkg_recipe_layer(int32_t cfg, int32_t layer, int32_t col0, int32_t co
   });
 }
 
+lkg_status lkg_gen_layer(uint64_t seed, int32_t in_dim, int32_t out_dim, int32_t segments, int32_t degree,
+                         double* bp, double* coeffs, double* bs, double* ss, double* os) {
+  return guarded([&] {
+    if (segments < 1) fail(LKG_ERR_CONFIG, "segments must be >= 1");  // model_gen.cpp:8
+    if (degree < 0) fail(LKG_ERR_CONFIG, "degree must be >= 0");
+    if (in_dim < 1 || out_dim < 1) fail(LKG_ERR_CONFIG, "layer dims must be >= 1");
+    need(bp, "breakpoints");
+    need(coeffs, "coeffs");
+    need(bs, "base_scale");
+    need(ss, "spline_scale");
+    need(os, "out_scale");
+    lkg::gen_layer(seed, in_dim, out_dim, segments, degree, bp, coeffs, bs, ss, os);
+  });
+}
+
+lkg_status lkg_gen_inputs(uint64_t seed, int64_t n, int64_t dim, double lo, double hi, int32_t clip, double* X) {
+  return guarded([&] {
+    if (!(lo < hi)) fail(LKG_ERR_CONFIG, "input range must satisfy lo < hi");  // model_gen.cpp:35
+    if (n < 0 || dim < 0) fail(LKG_ERR_DIMENSION, "negative size");
+    if (n * dim > 0) need(X, "X");
+    lkg::gen_inputs(seed, n, dim, lo, hi, clip != 0, X);
+  });
+}
+
 lkg_status lkg_recipe_inputs(int32_t cfg, int64_t row0, int64_t rows, float* X) {
   return guarded([&] {
     if (rows > 0) need(X, "X");

@@ -163,6 +163,9 @@ int recipe_dims(int cfg, int* n_layers, int* dims, int* G, double* lo, double* h
 void recipe_layer(int cfg, int layer, int col0, int col1, double* bp, double* coeffs, double* bs,
                   double* ss, double* os);
 void recipe_inputs(int cfg, int64_t row0, int64_t rows, float* X);
+void gen_layer(uint64_t seed, int d, int m, int segments, int degree, double* bp, double* coeffs, double* bs,
+               double* ss, double* os);
+void gen_inputs(uint64_t seed, int64_t n, int64_t dim, double lo, double hi, bool clip, double* X);
 
 // Host Cox-de Boor (bit-exact restatement of spline.cpp:8-27,69-83) for compile tables.
 void knot_grid(const std::vector<double>& bp, int degree, std::vector<double>& ext);

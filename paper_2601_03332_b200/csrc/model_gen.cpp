@@ -133,6 +133,32 @@ void recipe_layer(int cfg, int layer, int col0, int col1, double* bp, double* co
   }
 }
 
+// gen_layer (model_gen.cpp:7-27): breakpoints -1 + 2k/G, one Rng(seed) stream, per edge R
+// coefficients normal(0, 0.1) then base, spline, out scales uniform(0.5, 1.5).
+void gen_layer(uint64_t seed, int d, int m, int segments, int degree, double* bp, double* coeffs, double* bs,
+               double* ss, double* os) {
+  for (int k = 0; k <= segments; k++) bp[k] = -1.0 + 2.0 * static_cast<double>(k) / segments;
+  Xoshiro rng(seed);
+  const int R = segments + degree;
+  const int64_t E = (int64_t)d * m;
+  for (int64_t e = 0; e < E; e++) {
+    for (int r = 0; r < R; r++) coeffs[e * R + r] = rng.normal(0.0, 0.1);
+    bs[e] = rng.uniform(0.5, 1.5);
+    ss[e] = rng.uniform(0.5, 1.5);
+    os[e] = rng.uniform(0.5, 1.5);
+  }
+}
+
+// gen_inputs (model_gen.cpp:33-45): standard normals, optionally clamped to [lo, hi].
+void gen_inputs(uint64_t seed, int64_t n, int64_t dim, double lo, double hi, bool clip, double* X) {
+  Xoshiro rng(seed);
+  for (int64_t t = 0; t < n * dim; t++) {
+    double x = rng.normal();
+    if (clip) x = x < lo ? lo : (hi < x ? hi : x);  // std::clamp
+    X[t] = x;
+  }
+}
+
 void recipe_inputs(int cfg, int64_t row0, int64_t rows, float* X) {
   const Recipe& r = recipe(cfg);
   Xoshiro g(r.seed ^ 0x5eed5eed5eed5eedull);  // input salt, sweep.cpp:25

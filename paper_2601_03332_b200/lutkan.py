@@ -885,6 +885,28 @@ def eval_accuracy(layer: KanLayerSpec, artifact: "LutLayerArtifact", X, engine: 
 
 
 # ------------------------------------------------------------------ recipes
+def gen_layer(seed: int, in_dim: int, out_dim: int, segments: int, degree: int = 3) -> KanLayerSpec:
+    """model_gen.cpp:7-27 (the reference's test-model generator)."""
+    R, E = segments + degree, in_dim * out_dim
+    bp, co = np.zeros(max(segments, 0) + 1), np.zeros(max(E * R, 0))
+    bs, ss, os_ = np.zeros(max(E, 0)), np.zeros(max(E, 0)), np.zeros(max(E, 0))
+    check(lib().lkg_gen_layer(seed, in_dim, out_dim, segments, degree,
+                              *[a.ctypes.data_as(_capi.f64p) for a in (bp, co, bs, ss, os_)]))
+    return KanLayerSpec(in_dim, out_dim, KnotGrid(bp, degree), co.reshape(E, R), bs, ss, os_)
+
+
+def gen_sanity_layer(seed: int) -> KanLayerSpec:
+    """model_gen.cpp:29-31."""
+    return gen_layer(seed, 10, 8, 8, 3)
+
+
+def gen_inputs(seed: int, n: int, dim: int, lo: float, hi: float, clip: bool) -> np.ndarray:
+    """model_gen.cpp:33-45: [n, dim] f64 standard normals, clamped to [lo, hi] when clip."""
+    X = np.zeros((n, dim))
+    check(lib().lkg_gen_inputs(seed, n, dim, lo, hi, int(clip), X.ctypes.data_as(_capi.f64p)))
+    return X
+
+
 def recipe_dims(cfg: int):
     nl, G = C.c_int32(), C.c_int32()
     dims = (C.c_int32 * 5)()

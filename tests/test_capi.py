@@ -87,3 +87,26 @@ def test_gpu_calls_fail_loudly_without_gpu(lk):
         pass
     with pytest.raises(lk.CudaError):
         lk.Engine(0)
+
+
+def test_gen_layer_and_inputs_match_reference(port, ref):
+    """gen_layer / gen_sanity_layer / gen_inputs (model_gen.cpp:7-45): the product's host
+    generator equals the reference's bit for bit (and the C port)."""
+    import paper_2601_03332_b200 as lk
+    for seed, d, m, K, deg in ((0, 10, 8, 8, 3), (7, 3, 5, 4, 2), (123, 1, 1, 1, 0)):
+        g = lk.gen_layer(seed, d, m, K, deg)
+        for o in (port, ref):
+            s = o.gen_layer(seed, d, m, K, deg)
+            assert np.array_equal(g.grid.breakpoints, s.breakpoints)
+            assert np.array_equal(g.coeffs.ravel(), np.asarray(s.coeffs).ravel())
+            for a, b in ((g.base_scale, s.base_scale), (g.spline_scale, s.spline_scale), (g.out_scale, s.out_scale)):
+                assert np.array_equal(a, b)
+    for clip in (False, True):
+        X = lk.gen_inputs(5, 100, 7, -1.2, 1.1, clip)
+        for o in (port, ref):
+            assert np.array_equal(X, o.gen_inputs(5, 100, 7, -1.2, 1.1, clip))
+    assert lk.gen_sanity_layer(3).coeffs.shape == (80, 11)
+    with pytest.raises(lk.ConfigError):
+        lk.gen_inputs(1, 2, 2, 1.0, 1.0, True)
+    with pytest.raises(lk.ConfigError):
+        lk.gen_layer(1, 2, 2, 0, 3)
