@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   const int K = a.cc.K, L = a.cc.L;  // knots are uniformly spaced (tiled_eligible)
   uint32_t oob_inputs = 0, oob_rows = 0, oob2_inputs = 0, oob2_rows = 0;
   bool nonfinite = false, nonfinite2 = false;
-  float nfacc = 0.0f;
+  float nfacc = 0.0f, nfacc2 = 0.0f;
   int64_t g = 0;
   const int64_t x_rs = a.x_blk > 0 ? a.x_blk : a.d;  // row stride of the input layout
   // x tiles (64 rows x 8 inputs per warp) go global -> shared with 4-byte cp.async, transposed to
@@ -394,44 +394,54 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       }
       if (lane + 32 * r < rows_left) {
         if (FUSE) {
-          // next layer (runtime.cpp:298-314 chain) on this row's hidden activations out[0..m)
-          const int K2 = a.cc2.K, L2 = a.cc2.L, MP2 = a.MP2;
-          const float* CB2 = reinterpret_cast<const float*>(lut2 + a.cb_off2);
-          float y2[8];
-#pragma unroll
-          for (int j = 0; j < 8; j++) y2[j] = 0.0f;
+          // next layer (runtime.cpp:298-314 chain) on this row's hidden activations out[0..m):
+          // its whole value table is in shared memory (small layout, 2 outputs, MP2 == 2);
+          // inputs in pairs with both fast coordinate chains side by side
+          const int K2 = a.cc2.K, L2 = a.cc2.L;
+          const float2* V2 = reinterpret_cast<const float2*>(lut2);
+          const float2* CB2 = reinterpret_cast<const float2*>(lut2 + a.cb_off2);
+          float2 y2 = make_float2(0.f, 0.f);
           bool r_oob2 = false;
 #pragma unroll
-          for (int i2 = 0; i2 < 16; i2++) {
+          for (int i2 = 0; i2 < 16; i2 += 2) {
             if (i2 < a.m) {
-              const float h = out[i2];
-              const lkg::Coord c2 = lkg::lut_coords_fast(a.cc2, ktab2, h);
-              nonfinite2 |= !(fabsf(h) <= 3.402823466e38f);
-              oob2_inputs += (uint32_t)!c2.in;
-              r_oob2 |= !c2.in;
-              const bool tab = !(ZS && !c2.in);
-              float bx2 = 0.0f;
-              if (SR) {
-                const float xb = ZS ? h : c2.xp;
-                bx2 = lkg::silu_fast(xb);
+              const float h0 = out[i2], h1 = i2 + 1 < a.m ? out[i2 + 1] : a.cc2.lo;
+              bool s0, s1;
+              lkg::Coord c0 = lkg::lut_coords_fast_nb(a.cc2, ktab2, h0, s0);
+              lkg::Coord c1 = lkg::lut_coords_fast_nb(a.cc2, ktab2, h1, s1);
+              if (s0 || s1) {
+                if (s0) c0 = lkg::lut_coords(a.cc2, ktab2, h0);
+                if (s1) c1 = lkg::lut_coords(a.cc2, ktab2, h1);
               }
-              const int cell = i2 * K2 + c2.k, l1 = min(c2.l0 + 1, L2 - 1);
-              const float* V0 = reinterpret_cast<const float*>(lut2) + (cell * L2 + c2.l0) * MP2;
-              const float* V1 = reinterpret_cast<const float*>(lut2) + (cell * L2 + l1) * MP2;
-              const float w1 = c2.w1, w0 = 1.0f - w1;
+              nfacc2 = fmaf(h0, 0.0f, fmaf(h1, 0.0f, nfacc2));
+              const bool has1 = i2 + 1 < a.m;
+              oob2_inputs += (uint32_t)!c0.in + (uint32_t)(has1 && !c1.in);
+              r_oob2 |= !c0.in || (has1 && !c1.in);
 #pragma unroll
-              for (int j = 0; j < 8; j++) {
-                if (j < a.m2) {
-                  const float v = tab ? fmaf(w1, V1[j], w0 * V0[j]) : 0.0f;
-                  y2[j] += SR ? fmaf(CB2[i2 * MP2 + j], bx2, v) : v;
+              for (int t = 0; t < 2; t++) {
+                const lkg::Coord& c = t ? c1 : c0;
+                const float h = t ? h1 : h0;
+                if (t == 0 || has1) {
+                  const int ii = i2 + t;
+                  const bool tab = !(ZS && !c.in);
+                  const int cell = ii * K2 + c.k, l1 = min(c.l0 + 1, L2 - 1);
+                  const float2 v0 = V2[cell * L2 + c.l0], v1 = V2[cell * L2 + l1];
+                  const float w1 = c.w1, w0 = 1.0f - w1;
+                  float2 v = tab ? make_float2(fmaf(w1, v1.x, w0 * v0.x), fmaf(w1, v1.y, w0 * v0.y))
+                                 : make_float2(0.f, 0.f);
+                  if (SR) {
+                    const float bx2 = lkg::silu_fast(ZS ? h : c.xp);
+                    const float2 cb = CB2[ii];
+                    v = make_float2(fmaf(cb.x, bx2, v.x), fmaf(cb.y, bx2, v.y));
+                  }
+                  y2 = make_float2(y2.x + v.x, y2.y + v.y);
                 }
               }
             }
           }
           float* y2r = a.Y2 + row * a.m2;
-#pragma unroll
-          for (int j = 0; j < 8; j++)
-            if (j < a.m2) y2r[j] = y2[j];
+          y2r[0] = y2.x;
+          if (a.m2 > 1) y2r[1] = y2.y;
           oob2_rows += (uint32_t)r_oob2;
         } else {
           float* yr = a.Y + row * a.m + j0;
@@ -477,6 +487,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       if (orow2) atomicAdd(a.counters2 + 0, orow2);
       if (oi2) atomicAdd(a.counters2 + 1, oi2);
     }
+    nonfinite2 |= !(nfacc2 == 0.0f);
     if (__any_sync(0xffffffffu, nonfinite2) && lane == 0) atomicExch(a.counters2 + 2, 1ull);
   }
 }
@@ -958,13 +969,14 @@ static size_t tiled_smem(const lkg_layer* L, int W, int R) {
 
 bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
   // Off by default: measured on C2, the fused epilogue (16 coordinates per row at the end of
-  // each item, plus the second layer's state in the main kernel's registers) costs 0.20 ms per
-  // step against 0.07 ms for the separate fwd_small launch (1.59e12 vs 1.88e12 edge-evals/s).
+  // each item, all warps at once) costs 0.11 ms per step against 0.05 ms for the separate
+  // fwd_small launch (1.81e12 vs 1.99e12 edge-evals/s).
   // LKG_FUSE=1 re-enables it (kept for the C1-sized chains of SURVEY §8f rank 3).
   static const char* fz = getenv("LKG_FUSE");
   if (!fz || fz[0] != '1') return false;
   const TileGeom &g1 = L1->geom, &g2 = L2->geom;
   if (!g1.tile_bytes || g1.small || g1.codes_global || g1.n_jb != 1 || !g2.tile_bytes || g2.small != 2) return false;
+  if (g2.MP != 2) return false;  // the fused epilogue reads the value table as float2 (2 outputs)
   if (L1->in_dim > kFp32MaxD || L2->in_dim != L1->col1 - L1->col0 || L2->col1 - L2->col0 > 8) return false;
   if (L1->scheme != L2->scheme || L1->value_repr != L2->value_repr || L1->oob_policy != L2->oob_policy) return false;
   return tiled_smem(L1, kW, kR) + kMaxKT * 16 + ((g2.tile_bytes + 15) & ~15) <= 227 * 1024;
