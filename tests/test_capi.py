@@ -110,3 +110,28 @@ def test_gen_layer_and_inputs_match_reference(port, ref):
         lk.gen_inputs(1, 2, 2, 1.0, 1.0, True)
     with pytest.raises(lk.ConfigError):
         lk.gen_layer(1, 2, 2, 0, 3)
+
+
+def _build_c_demo(out):
+    """tests/cpp/c_abi_demo.c: plain C11 against include/lutkan_b200.h + liblutkan_b200.so."""
+    lib_dir = os.path.join(ROOT, "paper_2601_03332_b200")
+    cmd = ["gcc", "-std=c11", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+           os.path.join(ROOT, "tests", "cpp", "c_abi_demo.c"), "-o", str(out), "-L", lib_dir, "-llutkan_b200",
+           f"-Wl,-rpath,{lib_dir}", "-lm"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+
+
+def test_c_abi_compiles_from_plain_c(tmp_path):
+    """The boundary is a C ABI: a C11 program using it compiles warning-free and links."""
+    _build_c_demo(tmp_path / "c_abi_demo")
+    assert (tmp_path / "c_abi_demo").exists()
+
+
+@pytest.mark.gpu
+def test_c_abi_demo_runs_on_gpu(tmp_path):
+    """Compile, forward, save, reload, forward again, from C: identical outputs."""
+    exe = tmp_path / "c_abi_demo"
+    _build_c_demo(exe)
+    r = subprocess.run([str(exe), str(tmp_path / "demo.lut")], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, (r.stdout, r.stderr)
+    assert "reload identical 1" in r.stdout
