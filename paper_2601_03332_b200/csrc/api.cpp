@@ -214,6 +214,10 @@ lkg_status lkg_ctx_destroy(lkg_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->nccl) ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl));
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->comm_stream) {
+      cudaStreamSynchronize(ctx->comm_stream);
+      cudaStreamDestroy(ctx->comm_stream);
+    }
     if (ctx->copy_stream) {
       cudaStreamSynchronize(ctx->copy_stream);
       cudaStreamDestroy(ctx->copy_stream);
@@ -641,7 +645,10 @@ lkg_status lkg_model_forward_host(lkg_ctx* ctx, const lkg_layer* const* chain, i
     const int64_t d = chain[0]->in_dim, mo = chain[n - 1]->out_dim;
     // Row chunks of ~32 MB of X: the H2D copy of chunk c+1 (copy stream) overlaps the chain on
     // chunk c (context stream); two device input buffers, event-ordered.
-    const int64_t ch = std::max<int64_t>(65536, (32ll << 20) / (4 * d));
+    // Chunk starts are multiples of kRowAlign rows, so every row keeps its lane phase and the
+    // chunked path is bit-identical to one launch.
+    const int64_t ch = (std::max<int64_t>(65536, (32ll << 20) / (4 * d)) + lkg::kRowAlign - 1) / lkg::kRowAlign *
+                       lkg::kRowAlign;
     const int64_t nch = rows > ch ? (rows + ch - 1) / ch : 1, cr = nch > 1 ? ch : rows;
     const size_t xb = sizeof(float) * cr * d, yb = sizeof(float) * rows * mo;
     const size_t xstride = ((xb + 255) / 256) * 256;
@@ -1055,27 +1062,64 @@ lkg_status lkg_model_forward_sharded(lkg_ctx* ctx, const lkg_layer* const* chain
       ensure(ctx->scratch[0], sizeof(float) * rows * loc);
       ensure(ctx->gather, sizeof(float) * rows * full);
     }
-    const float* cur = X;
-    int32_t blk = 0;
+    // Row chunks pipeline the exchange: chunk c of layer l is all-gathered on the
+    // communication stream while layer l computes chunk c+1, and layer l+1 starts on chunk c as
+    // soon as its gather lands. Per chunk the gathered activations are rank-major blocks
+    // [G][rows_c][m_l] (ncclAllGather's layout), consumed in place by the next layer.
+    static const char* chunk_env = getenv("LKG_SHARD_CHUNKS");
+    int nch = chunk_env ? atoi(chunk_env) : (G > 1 && rows >= 8192 ? 4 : 1);
+    nch = (int)std::max<int64_t>(1, std::min<int64_t>(nch, std::max<int64_t>(rows, 1)));
+    const int64_t rc = ((rows + nch - 1) / nch + lkg::kRowAlign - 1) / lkg::kRowAlign * lkg::kRowAlign;
+    if (nch > 1 && n > 1 && !ctx->comm_stream)
+      LKG_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    cudaStream_t cs = nch > 1 ? ctx->comm_stream : ctx->stream;
+    std::vector<cudaEvent_t> events;
+    auto new_event = [&]() {
+      cudaEvent_t e;
+      LKG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      events.push_back(e);
+      return e;
+    };
+    std::vector<cudaEvent_t> gathered(nch, nullptr), prev_gathered(nch, nullptr);
     for (int l = 0; l < n; l++) {
       const bool last = l == n - 1;
-      float* dst = last ? Y : ctx->scratch[0].as<float>();
-      lkg::launch_forward(ctx, chain[l], cur, rows, blk, dst, l, true);
-      ctx->rows_seen[l] += (uint64_t)rows;
-      ctx->in_dim_seen[l] = chain[l]->in_dim;
-      if (!last) {
-        const size_t cnt = (size_t)rows * chain[l]->out_dim;
+      const int64_t m_l = chain[l]->out_dim, m_prev = l ? chain[l - 1]->out_dim : 0;
+      for (int c = 0; c < nch; c++) {
+        const int64_t r0 = c * rc, rn = std::min(rc, rows - r0);
+        if (rn <= 0) break;
+        const float* in = l == 0 ? X + r0 * chain[0]->in_dim : ctx->gather.as<float>() + (int64_t)G * r0 * m_prev;
+        if (l > 0 && nch > 1) LKG_CUDA(cudaStreamWaitEvent(ctx->stream, prev_gathered[c], 0));
+        float* dst = last ? Y + r0 * m_l : ctx->scratch[0].as<float>() + r0 * m_l;
+        lkg::launch_forward(ctx, chain[l], in, rn, l == 0 ? 0 : (int32_t)m_prev, dst, l, true);
+        if (last) continue;
+        if (nch > 1) {
+          const cudaEvent_t done = new_event();
+          LKG_CUDA(cudaEventRecord(done, ctx->stream));
+          LKG_CUDA(cudaStreamWaitEvent(cs, done, 0));
+        }
+        float* gdst = ctx->gather.as<float>() + (int64_t)G * r0 * m_l;
+        const size_t cnt = (size_t)rn * m_l;
         if (ctx->nccl) {
-          const ncclResult_t r = ncclAllGather(dst, ctx->gather.p, cnt, ncclFloat, static_cast<ncclComm_t>(ctx->nccl),
-                                               ctx->stream);
+          const ncclResult_t r = ncclAllGather(dst, gdst, cnt, ncclFloat, static_cast<ncclComm_t>(ctx->nccl), cs);
           if (r != ncclSuccess) fail(LKG_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
         } else {
-          LKG_CUDA(cudaMemcpyAsync(ctx->gather.p, dst, sizeof(float) * cnt, cudaMemcpyDeviceToDevice, ctx->stream));
+          LKG_CUDA(cudaMemcpyAsync(gdst, dst, sizeof(float) * cnt, cudaMemcpyDeviceToDevice, cs));
         }
-        cur = ctx->gather.as<float>();
-        blk = chain[l]->out_dim;  // rank-major blocks of the gathered activations
+        if (nch > 1) {
+          gathered[c] = new_event();
+          LKG_CUDA(cudaEventRecord(gathered[c], cs));
+        }
       }
+      ctx->rows_seen[l] += (uint64_t)rows;
+      ctx->in_dim_seen[l] = chain[l]->in_dim;
+      prev_gathered.swap(gathered);
     }
+    if (nch > 1 && n > 1) {  // the caller's stream sees every gather (and nothing outlives the call)
+      const cudaEvent_t tail = new_event();
+      LKG_CUDA(cudaEventRecord(tail, cs));
+      LKG_CUDA(cudaStreamWaitEvent(ctx->stream, tail, 0));
+    }
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
     if (stats) collect_impl(ctx, stats, n);
   });
 }

@@ -11,6 +11,12 @@
 
 namespace lkg {
 
+// Row splits (host-path chunks, sharded-chain chunks, batch shards) start at multiples of this:
+// the kernels walk a row's inputs in a lane-dependent rotation (row mod 32 at most), so a row's
+// fp32 accumulation order -- and its last bits -- depend on its position modulo 32. Aligned
+// splits keep every row bit-identical to the single-launch result.
+constexpr int64_t kRowAlign = 64;
+
 // Thread-local last error (lkg_last_error).
 void set_error(const std::string& msg);
 
@@ -113,6 +119,7 @@ struct lkg_ctx {
   lkg::DBuf hostio;      // device staging for lkg_model_forward_host
   cudaStream_t copy_stream = nullptr;  // H2D of the next chunk overlaps the chain on `stream`
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+  cudaStream_t comm_stream = nullptr;  // sharded chain: all-gathers overlap the next chunk's compute
   void* nccl = nullptr;  // ncclComm_t
   int32_t nranks = 1, rank = 0;
 };

@@ -27,11 +27,19 @@ from .lutkan import (ConfigError, DimensionError, Engine, KanLayerSpec, LutLayer
                      QuantConfig, check, compile_layer)
 
 
+ROW_ALIGN = 64  # csrc/lkg_internal.h kRowAlign: shard starts keep every row's lane phase
+
+
 def batch_bounds(rows: int, world: int, rank: int) -> tuple[int, int]:
-    """Rows [r0, r1) of `rank` under batch sharding (balanced, contiguous)."""
+    """Rows [r0, r1) of `rank` under batch sharding: contiguous, balanced to within ROW_ALIGN rows,
+    every shard starting at a multiple of ROW_ALIGN so each row's result is bit-identical to the
+    1-GPU run."""
     if not 0 <= rank < world:
         raise ValueError("rank out of range")
-    return rows * rank // world, rows * (rank + 1) // world
+
+    def start(r):
+        return min(rows, (rows * r // world + ROW_ALIGN - 1) // ROW_ALIGN * ROW_ALIGN)
+    return start(rank), (rows if rank == world - 1 else start(rank + 1))
 
 
 def column_bounds(m: int, world: int, rank: int) -> tuple[int, int]:
