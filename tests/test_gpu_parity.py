@@ -582,3 +582,37 @@ def test_element_primitives_spline_and_quantize(lk, oracle):
         lk.quantize_segment_symmetric([1.0, np.inf])
     with pytest.raises(lk.ConfigError):
         lk.quantize_segment_asymmetric([])
+
+
+# ------------------------------------------------------------------ randomized shapes
+@pytest.mark.parametrize("seed", range(80))
+def test_fuzz_compile_and_forward(lk, oracle, seed):
+    """Random layer shapes, grids and contracts (d, m off the 8/16 tile multiples; K up to 40;
+    L from 2 to 160; uneven knots; phi and spline_component; f16 params; all boundary/OOB
+    contracts; ragged rows): compile byte-identical, forward within the bar, stats exact."""
+    from oracle.pyoracle import Spec
+    rng = np.random.default_rng(1000 + seed)
+    d = int(rng.choice([1, 3, 7, 9, 17, 33, 70, 130, 300]))
+    m = int(rng.choice([1, 2, 5, 8, 9, 15, 16, 17, 40]))
+    K = int(rng.integers(1, 41))
+    deg = int(rng.integers(1, 4))
+    L = int(rng.choice([2, 3, 16, 33, 64, 100, 160]))
+    uniform = rng.random() < 0.7
+    lo, hi = sorted(rng.uniform(-3, 3, 2)) if rng.random() < 0.5 else (-1.0, 1.0)
+    if hi - lo < 0.5:
+        hi = lo + 0.5
+    bp = np.linspace(lo, hi, K + 1) if uniform else np.cumsum(rng.uniform(0.2, 1.0, K + 1)) * (hi - lo) / (K + 1) + lo
+    E, R = d * m, K + deg
+    so = Spec(d, m, bp, rng.normal(0, 0.3, (E, R)), rng.uniform(-1, 1, E), rng.uniform(0.5, 1.5, E),
+              rng.uniform(0.5, 1.5, E), deg)
+    scheme, vr, pd = int(rng.integers(0, 2)), int(rng.random() < 0.8), int(rng.random() < 0.25)
+    bm, op = int(rng.integers(0, 2)), int(rng.integers(0, 2))
+    ao = oracle.compile_layer(so, L, scheme, vr, pd, bm, op)
+    spec = to_product_spec(lk, so)
+    qc = lk.QuantConfig(L, lk.Scheme(scheme), lk.Dtype(scheme), lk.ValueRepr(vr), lk.Interp.Linear, lk.ParamDtype(pd))
+    g = lk.compile_layer(spec, qc, lk.OobConfig(lk.BoundaryMode(bm), lk.OobPolicy(op)))
+    assert _bytes_equal(g.q_table, ao.q) and _bytes_equal(g.scale, ao.scale) and _bytes_equal(g.y_min, ao.y_min)
+    rows = int(rng.choice([1, 37, 1000, 2500]))
+    X = rng.uniform(lo - 0.3 * (hi - lo), hi + 0.3 * (hi - lo), (rows, d)).astype(np.float32)
+    X.ravel()[:: max(1, X.size // 50)] = np.asarray(ao.knots)[rng.integers(0, K + 1, X.ravel()[:: max(1, X.size // 50)].size)]
+    _layer_parity(lk, oracle, ao, X, f"fuzz {seed}: d{d} m{m} K{K} deg{deg} L{L} s{scheme} vr{vr} pd{pd} bm{bm} op{op}")
