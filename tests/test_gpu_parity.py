@@ -616,3 +616,27 @@ def test_fuzz_compile_and_forward(lk, oracle, seed):
     X = rng.uniform(lo - 0.3 * (hi - lo), hi + 0.3 * (hi - lo), (rows, d)).astype(np.float32)
     X.ravel()[:: max(1, X.size // 50)] = np.asarray(ao.knots)[rng.integers(0, K + 1, X.ravel()[:: max(1, X.size // 50)].size)]
     _layer_parity(lk, oracle, ao, X, f"fuzz {seed}: d{d} m{m} K{K} deg{deg} L{L} s{scheme} vr{vr} pd{pd} bm{bm} op{op}")
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_fuzz_spline_forward(lk, oracle, seed):
+    """Random spline layers through layer_forward_batch (tiled kernel on uniform cubic grids,
+    generic kernel otherwise) against the reference's spline forward."""
+    import dataclasses
+    from oracle.pyoracle import Spec
+    rng = np.random.default_rng(5000 + seed)
+    d = int(rng.choice([1, 5, 8, 13, 64, 300]))
+    m = int(rng.choice([1, 3, 16, 17, 33]))
+    K = int(rng.integers(1, 30))
+    deg = 3 if rng.random() < 0.6 else int(rng.integers(0, 6))
+    uniform = rng.random() < 0.7
+    bp = np.linspace(-1.5, 2.0, K + 1) if uniform else np.cumsum(rng.uniform(0.1, 1.0, K + 1)) - 1.0
+    E, R = d * m, K + deg
+    so = Spec(d, m, bp, rng.normal(0, 0.4, (E, R)), rng.uniform(-1, 1, E), rng.uniform(0.5, 1.5, E),
+              rng.uniform(0.5, 1.5, E), deg)
+    spec = to_product_spec(lk, so)
+    rows = int(rng.choice([1, 40, 700, 2100]))
+    X = rng.uniform(bp[0] - 1.0, bp[-1] + 1.0, (rows, d)).astype(np.float32)
+    Y = lk.layer_forward_batch(spec, X)
+    Yo = oracle.spline_forward(so, X.astype(np.float64))
+    assert_close(Y, Yo, f"spline fuzz {seed}: d{d} m{m} K{K} deg{deg} uniform{uniform}")
