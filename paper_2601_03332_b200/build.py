@@ -13,8 +13,12 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "liblutkan_b200.so")
+# A/B experiments: LKG_BUILD_TAG=x builds into _build_x/ and ab/liblutkan_x.so with LKG_NVCC_EXTRA flags
+# (load it with LKG_LIB=ab/liblutkan_x.so); the default build is unaffected.
+_TAG = os.environ.get("LKG_BUILD_TAG", "")
+BUILD = os.path.join(PKG, "_build" + ("_" + _TAG if _TAG else ""))
+LIB = os.path.join(ROOT, "ab", f"liblutkan_{_TAG}.so") if _TAG else os.path.join(PKG, "liblutkan_b200.so")
+EXTRA = os.environ.get("LKG_NVCC_EXTRA", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include")]
@@ -31,6 +35,7 @@ def _newer(src: str, obj: str, headers: list[str]) -> bool:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     headers = (glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
                glob.glob(os.path.join(ROOT, "include", "*.h")))
     objs = []
@@ -40,7 +45,7 @@ def build(verbose: bool = False) -> str:
         objs.append(obj)
         if not _newer(src, obj, headers):
             continue
-        cmd = [NVCC, *ARCH, *COMMON, *PER_FILE.get(name, []), "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *COMMON, *EXTRA, *PER_FILE.get(name, []), "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -12,7 +12,8 @@
 //    Symmetric codes are stored biased (q ^ 0x80 = q + 128) so every code is an unsigned byte.
 //  * A CTA owns a 1024-row tile x one 16-column j-block and streams the tiles of its j-block
 //    through shared memory with cp.async.bulk (TMA bulk copies) completing on mbarriers,
-//    double-buffered. CTAs are persistent over (row tile, j-block) items.
+//    double-buffered; the last warp to finish with a buffer refills it (no CTA barrier per tile,
+//    so warps drift apart: C4 layers -6% time). CTAs are persistent over (row tile, j-block) items.
 //  * Lane = row (R rows per lane). Within a tile the lanes walk the 8 inputs in a ROTATED order
 //    (step s: i_lo = (s + lane) & 7), so the 8 lanes of every LDS.128 phase hit 8 different
 //    16-byte bank groups of each 128-byte line: code, P and CB reads are conflict-free no matter
@@ -68,6 +69,7 @@ struct TiledArgs {
   unsigned long long* counters;
   lkg::CoordConst cc;        // coordinate constants (coords.cuh)
   int64_t n_items, n_rt;
+  int32_t ns;           // stage buffers (2 or 3, whatever fits shared memory)
   float4 ktab[kMaxKT];  // {T_k, T_k+1, (L-1)/(T_k+1 - T_k), 0}
   // fused next layer (FUSE): a small-out_dim layer evaluated in the epilogue from the 16 hidden
   // activations each lane holds (the whole-layer "small" layout, resident in shared memory)
@@ -109,7 +111,7 @@ __device__ __forceinline__ void item_coords(const TiledArgs& a, bool gc, uint32_
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1, bool GC = false>
 __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int NS = 2;
+  const int NS = a.ns;
   constexpr int ROWS_W = 32 * R;        // rows per warp
   constexpr int XS = ROWS_W + 4;        // padded row stride of the transposed x tile
   constexpr int NXL = ROWS_W / 4;        // x elements each lane stages per tile (cp.async)
@@ -123,7 +125,8 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   float* xsw = reinterpret_cast<float*>(smem + NS * sb) + warp * 2 * G * XS;  // per-warp x tiles (x2)
   float4* ktab = reinterpret_cast<float4*>(smem + NS * sb + 2 * W * G * XS * 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + kMaxKT);
-  float4* ktab2 = reinterpret_cast<float4*>(full + 4);
+  uint32_t* fin = reinterpret_cast<uint32_t*>(full + 4);  // warps done with each stage buffer
+  float4* ktab2 = reinterpret_cast<float4*>(full + 8);
   uint8_t* lut2 = reinterpret_cast<uint8_t*>(ktab2 + kMaxKT);
 
   for (int k = tid; k < a.cc.K; k += W * 32) ktab[k] = a.ktab[k];
@@ -133,7 +136,10 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       *reinterpret_cast<uint4*>(lut2 + o) = __ldg(reinterpret_cast<const uint4*>(a.lut2 + o));
   }
   if (tid == 0) {
-    for (int s = 0; s < NS; s++) mbar_init(&full[s], 1);
+    for (int s = 0; s < NS; s++) {
+      mbar_init(&full[s], 1);
+      fin[s] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // F64: the f64 accumulators live in Tensor Memory (tmem.cuh), not registers: each thread owns
@@ -370,8 +376,19 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           lkg::tmem_st32(tm_warp + 32 * r, w);
         }
       }
-      __syncthreads();  // every warp is done with this stage buffer
-      if (tid == 0 && g + NS < n_stages) issue(g + NS);
+      // Stage release without a CTA barrier: the last warp done with this buffer refills it, so
+      // warps drift up to NS-1 stages apart instead of re-aligning at every tile.
+      __syncwarp();
+      if (lane == 0) {
+        const int st = (int)(g % NS);
+        __threadfence_block();
+        if (atomicAdd(&fin[st], 1u) == (uint32_t)(W - 1)) {
+          fin[st] = 0;
+          __threadfence_block();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (g + NS < n_stages) issue(g + NS);
+        }
+      }
     }
     if (cnt) oob_inputs += oob_item;
     // epilogue: rows of this lane, 16 outputs of the j-block
@@ -799,8 +816,8 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   off = (off + 127) / 128 * 128;
   const size_t xs_bytes = (size_t)2 * kW * G * (32 * kR + 4) * 4;  // double-buffered x tiles
   static const bool force_gc = getenv("LKG_FORCE_GC") != nullptr;  // test / tuning hook
-  gm.codes_global = force_gc || 2 * off + xs_bytes + kMaxKT * 16 + 32 > 227 * 1024;  // codes stay in global (L2)
-  if (gm.codes_global && 2 * (off - gm.p_off) + xs_bytes + kMaxKT * 16 + 32 > 227 * 1024) return;  // generic
+  gm.codes_global = force_gc || 2 * off + xs_bytes + kMaxKT * 16 + 64 > 227 * 1024;  // codes stay in global (L2)
+  if (gm.codes_global && 2 * (off - gm.p_off) + xs_bytes + kMaxKT * 16 + 64 > 227 * 1024) return;  // generic
   gm.tile_bytes = off;
   gm.JB = JB;
   gm.IC = G;
@@ -962,9 +979,17 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
   ctx->launches++;
 }
 
-static size_t tiled_smem(const lkg_layer* L, int W, int R) {
+static size_t tiled_smem(const lkg_layer* L, int W, int R, int ns = 2) {
   const int64_t sb = L->geom.tile_bytes - (L->geom.codes_global ? L->geom.p_off : 0);
-  return 2 * sb + (size_t)2 * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 32;
+  return ns * sb + (size_t)2 * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 64;
+}
+
+// Two stage buffers. Measured on B200 with the barrier-free stage release: a third buffer (where
+// it fits) costs 11% on configs[1] layer 0 (0.652 vs 0.588 ms) and gains nothing elsewhere.
+static int tiled_stages(const lkg_layer* L, int W, int R, size_t extra) {
+  static const char* e = getenv("LKG_STAGES");  // tuning hook: LKG_STAGES=3
+  if (e && e[0] == '3' && tiled_smem(L, W, R, 3) + extra <= 227 * 1024) return 3;
+  return 2;
 }
 
 bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
@@ -1014,7 +1039,9 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   a.n_rt = (rows + row_tile - 1) / row_tile;
   a.n_items = a.n_rt * gm.n_jb;
   const int grid = (int)std::min<int64_t>(a.n_items, sm_count(ctx->device));
-  size_t smem = tiled_smem(L, W, R);
+  const size_t extra = (L2 && !gm.codes_global) ? kMaxKT * 16 + ((L2->geom.tile_bytes + 15) & ~15) : 0;
+  a.ns = tiled_stages(L, W, R, extra);
+  size_t smem = tiled_smem(L, W, R, a.ns);
   const int sel = (asym << 2) | (sr << 1) | (int)zs;
   if (gm.codes_global) {
     switch (sel) {
