@@ -50,9 +50,12 @@ WORKLOADS = {
     "c2": (2, 1_000_000, 64, 0, 1, 0),    # configs[1], int8 symmetric
     "c2a": (2, 1_000_000, 64, 1, 1, 0),   # configs[1], uint8 asymmetric
     "c3": (3, 262_144, 64, 0, 0, 0),      # configs[2] cell L=64 sym half_open clip_x
-    "c4": (4, 65_536, 64, 0, 0, 0),       # configs[3] (row count reduced per step)
+    "c4": (4, 1_048_576, 64, 0, 0, 0),    # configs[3]: the full batch, sharded over the ranks
     "c5": (5, 16_384, 128, 1, 1, 1),      # configs[4]: column-sharded over the ranks, NCCL all-gather
 }
+# workloads whose BASELINE batch is fixed and split over the GPUs (strong scaling); the others give
+# every rank its own full batch (weak scaling)
+STRONG = {"c4"}
 SMEM_PEAK_GBS = 36600.0  # measured conflict-free LDS.128 throughput, tools/microbench (148 SMs)
 BYTES_PER_EE = {0: 6.0, 1: 10.0}  # algorithmic smem bytes per edge-eval
 
@@ -311,9 +314,16 @@ def main():
     from paper_2601_03332_b200._capi import OobStatsC, lib
     handles = (C.c_void_p * nl)(*[d.handle for d in dev])
 
-    # this rank's batch: rows [rank*rows, (rank+1)*rows) of the recipe stream, pinned host + device copy
+    # this rank's batch, pinned host + device copy: weak scaling -> rows [rank*rows, (rank+1)*rows) of
+    # the recipe stream; strong scaling (c4) -> this rank's batch shard of the fixed batch
+    if args.workload in STRONG:
+        from paper_2601_03332_b200.sharding import batch_bounds
+        r0, r1 = batch_bounds(rows, world, rank)
+        total_rows, rows = rows, r1 - r0
+    else:
+        r0, total_rows = rank * rows, world * rows
     Xh = torch.empty((rows, dims[0]), dtype=torch.float32).pin_memory()
-    lk.recipe_inputs(cfg, rank * rows, rows, out=Xh.numpy())
+    lk.recipe_inputs(cfg, r0, rows, out=Xh.numpy())
     Xd = Xh.to(f"cuda:{local}", non_blocking=False)
     Yd = torch.empty((rows, dims[-1]), dtype=torch.float32, device=f"cuda:{local}")
     Yh = torch.empty((rows, dims[-1]), dtype=torch.float32).pin_memory()
@@ -347,7 +357,7 @@ def main():
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    value = world * rows * ee_row / (ms * 1e-3)
+    value = total_rows * ee_row / (ms * 1e-3)
 
     # dominant kernel. When the whole chain is one launch per step (C2: layer 1 fused into layer 0's
     # epilogue) it is that launch, timed by the step events above; otherwise the largest layer,
@@ -430,19 +440,21 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         ms_e = float(te.item())
         eng.collect(nl)
-        e2e = {"value": world * rows * ee_row / (ms_e * 1e-3), "unit": "edge-evals/s",
+        e2e = {"value": total_rows * ee_row / (ms_e * 1e-3), "unit": "edge-evals/s",
                "h2d_bytes_per_step": rows * dims[0] * 4, "d2h_bytes_per_step": rows * dims[-1] * 4,
                "ms_per_step": ms_e}
 
     if rank == 0:
         line = {"metric": "LUT-KAN forward edge-evals/s (batch x sum d*m)", "value": value, "unit": "edge-evals/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/i8 codes, fp32 math",
+                "higher_is_better": True, "scaling": "strong" if args.workload in STRONG else "weak",
+                "vs_baseline": None, "dtype": "u8/i8 codes, fp32 math",
                 "data": "synthetic (BASELINE.json recipe, reference Rng; inputs > L2, no flush)",
                 "config": {"workload": args.workload, "cfg": f"configs[{cfg - 1}]", "dims": dims, "G": G, "L": L,
                            "scheme": ["int8_symmetric", "uint8_asymmetric"][scheme],
                            "boundary_mode": ["half_open", "closed"][bm], "oob_policy": ["clip_x", "zero_spline"][op],
-                           "rows_per_gpu": rows, "parallelism": f"batch dp{world}, LUT replicated",
+                           "rows": total_rows, "rows_per_gpu": rows,
+                           "parallelism": f"batch dp{world}, LUT replicated",
                            "l2": "inputs larger than L2 (no flush)"},
                 "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
                 "oob_any_frac_layer0": stats[0].oob_any_frac(), "clocks": clk.summary(),

@@ -213,6 +213,11 @@ lkg_status lkg_artifact_load(lkg_ctx* ctx, const char* path, lkg_layer** out);
  * load validation of a file without an upload (returns the status load would return). */
 lkg_status lkg_artifact_save_desc(const lkg_layer_desc* desc, const char* path, int32_t mode);
 lkg_status lkg_artifact_check(const char* path);
+/* artifact_manifest_json (artifact_io.hpp:66-67, artifact_io.cpp:98-124): the manifest text exactly
+ * as save_artifact writes it. Reads only the descriptor's shape and enum fields (no array). Writes
+ * at most cap-1 bytes plus a NUL into buf (buf may be NULL to query the length) and the full
+ * length into *len. Host-only. */
+lkg_status lkg_artifact_manifest(const lkg_layer_desc* desc, char* buf, size_t cap, size_t* len);
 
 /* ---------------------------------------------- element primitives (§8a) */
 /* The reference's scalar functions, batched on the device in f64 with the reference's
@@ -246,6 +251,10 @@ lkg_status lkg_eval_accuracy(lkg_ctx* ctx, const lkg_spec* spec, const lkg_layer
 /* Same with a HOST X buffer. */
 lkg_status lkg_eval_accuracy_host(lkg_ctx* ctx, const lkg_spec* spec, const lkg_layer* layer,
                                   const float* X_host, int64_t rows, lkg_eval_report* out);
+/* Same with a HOST f64 X buffer (the reference's Matrix values, not rounded to fp32): the reports
+ * of the sweep driver, whose inputs are gen_inputs' f64 normals (sweep.cpp:87-90). */
+lkg_status lkg_eval_accuracy_host_f64(lkg_ctx* ctx, const lkg_spec* spec, const lkg_layer* layer,
+                                      const double* X_host, int64_t rows, lkg_eval_report* out);
 
 /* ------------------------------------------------ multi-GPU (column shards) */
 /* NCCL communicator for output-column sharding. id: 128 bytes from

@@ -321,9 +321,9 @@ inline lutkan::EvalReport eval_accuracy(const lutkan::KanLayerSpec& layer, const
     throw lutkan::DimensionError("layer and artifact shapes differ");
   if (X.cols != static_cast<size_t>(layer.in_dim()))
     throw lutkan::DimensionError("input column count does not match in_dim");
-  std::vector<float> x(X.data.begin(), X.data.end());
-  lkg_eval_report r{};
-  check(lkg_eval_accuracy_host(ctx.get(), ctx.spec(layer), ctx.layer(a), x.data(), static_cast<int64_t>(X.rows), &r));
+  lkg_eval_report r{};  // the Matrix's f64 values, unrounded (eval_accuracy is not a hot path)
+  check(lkg_eval_accuracy_host_f64(ctx.get(), ctx.spec(layer), ctx.layer(a), X.data.data(),
+                                   static_cast<int64_t>(X.rows), &r));
   lutkan::EvalReport e;
   e.quant.samples_per_segment = a.L;
   e.quant.scheme = a.scheme;

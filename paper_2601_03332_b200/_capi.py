@@ -97,6 +97,7 @@ SIGNATURES = {
     "lkg_artifact_load": (C.c_int, [C.c_void_p, C.c_char_p, _P(C.c_void_p)]),
     "lkg_artifact_save_desc": (C.c_int, [_P(LayerDesc), C.c_char_p, C.c_int32]),
     "lkg_artifact_check": (C.c_int, [C.c_char_p]),
+    "lkg_artifact_manifest": (C.c_int, [_P(LayerDesc), C.c_char_p, C.c_size_t, _P(C.c_size_t)]),
     "lkg_lut_coords64": (C.c_int, [C.c_void_p, C.c_void_p, f64p, C.c_int64, u8p, f64p, i32p, i32p, i32p, f64p]),
     "lkg_lut_eval": (C.c_int, [C.c_void_p, C.c_void_p, i32p, f64p, C.c_int64, f64p, u8p, f64p]),
     "lkg_basis_values": (C.c_int, [C.c_void_p, f64p, C.c_int32, C.c_int32, f64p, C.c_int64, f64p]),
@@ -105,6 +106,8 @@ SIGNATURES = {
     "lkg_eval_accuracy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, _P(EvalReportC)]),
     "lkg_eval_accuracy_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                          _P(EvalReportC)]),
+    "lkg_eval_accuracy_host_f64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                             _P(EvalReportC)]),
     "lkg_nccl_unique_id": (C.c_int, [_P(C.c_uint8)]),
     "lkg_ctx_init_nccl": (C.c_int, [C.c_void_p, _P(C.c_uint8), C.c_int32, C.c_int32]),
     "lkg_model_forward_sharded": (C.c_int, [C.c_void_p, _P(C.c_void_p), C.c_int32, C.c_void_p, C.c_int64,

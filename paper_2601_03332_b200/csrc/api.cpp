@@ -939,8 +939,8 @@ lkg_status lkg_quantize_segments(lkg_ctx* ctx, const double* v, int64_t nseg, in
 }
 
 // ---------------------------------------------------------------- eval_accuracy
-static void eval_impl(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const float* X, int64_t rows,
-                      lkg_eval_report* out) {
+static void eval_impl(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const void* X, bool x_f64,
+                      int64_t rows, lkg_eval_report* out) {
   // metrics.cpp:32-35
   if (S->in_dim != L->in_dim || S->col1 - S->col0 != L->col1 - L->col0 || S->col0 != L->col0)
     fail(LKG_ERR_DIMENSION, "layer and artifact shapes differ");
@@ -954,7 +954,7 @@ static void eval_impl(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const
     LKG_CUDA(cudaMemsetAsync(acc.p, 0, acc.bytes, ctx->stream));
     double* dsum = acc.as<double>();
     unsigned long long* u = reinterpret_cast<unsigned long long*>(dsum + 2);
-    lkg::launch_eval(ctx, S, L, X, rows, dsum, u);
+    lkg::launch_eval(ctx, S, L, X, x_f64, rows, dsum, u);
     double hs[2];
     unsigned long long hu[8];
     LKG_CUDA(cudaMemcpyAsync(hs, dsum, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
@@ -987,7 +987,7 @@ lkg_status lkg_eval_accuracy(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L
     if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
     if (rows > 0) need(X, "X");
     DeviceGuard g(ctx->device);
-    eval_impl(ctx, S, L, X, rows, out);
+    eval_impl(ctx, S, L, X, false, rows, out);
   });
 }
 
@@ -1005,7 +1005,25 @@ lkg_status lkg_eval_accuracy_host(lkg_ctx* ctx, const lkg_spec* S, const lkg_lay
     ensure(ctx->hostio, xb + 256);
     float* dX = ctx->hostio.as<float>();
     if (rows > 0) LKG_CUDA(cudaMemcpyAsync(dX, Xh, xb, cudaMemcpyHostToDevice, ctx->stream));
-    eval_impl(ctx, S, L, dX, rows, out);
+    eval_impl(ctx, S, L, dX, false, rows, out);
+  });
+}
+
+lkg_status lkg_eval_accuracy_host_f64(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const double* Xh,
+                                      int64_t rows, lkg_eval_report* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(S, "spec");
+    need(L, "layer");
+    need(out, "out");
+    if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
+    if (rows > 0) need(Xh, "X");
+    DeviceGuard g(ctx->device);
+    const size_t xb = sizeof(double) * rows * S->in_dim;
+    ensure(ctx->hostio, xb + 256);
+    double* dX = ctx->hostio.as<double>();
+    if (rows > 0) LKG_CUDA(cudaMemcpyAsync(dX, Xh, xb, cudaMemcpyHostToDevice, ctx->stream));
+    eval_impl(ctx, S, L, dX, true, rows, out);
   });
 }
 

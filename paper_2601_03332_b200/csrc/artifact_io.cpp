@@ -587,16 +587,10 @@ struct ZipWriter {
 
 
 // ---------------------------------------------------------------------------- writer
-// save_artifact's container (artifact_io.cpp:206-219 + zip.cpp:80-136) from host arrays.
-// mode: 0 the reference's archive (byte-identical), 1 stored entries, 2 parallel-inflate deflate
-void write_container(const lkg_layer_desc& d, const char* path, int mode) {
-  const bool store = mode == 1;
-  // sizes/offsets at or above `lim` get ZIP64 records; LKG_ZIP64_FORCE=1 (test hook) forces them
-  static const bool force64 = std::getenv("LKG_ZIP64_FORCE") != nullptr;
-  const uint64_t lim = force64 ? 0 : kMax32;
+// The manifest (artifact_io.cpp:98-124) exactly as save_artifact writes it: nlohmann dump(2).
+std::string manifest_text(const lkg_layer_desc& d) {
   const int64_t E = (int64_t)d.in_dim * d.out_dim, K = d.K, Ls = d.L;
-  const bool sr = d.value_repr == LKG_REPR_SPLINE_COMPONENT, f16 = d.param_dtype == LKG_PARAM_F16;
-  // manifest (artifact_io.cpp:98-124), dumped as nlohmann dump(2)
+  const bool sr = d.value_repr == LKG_REPR_SPLINE_COMPONENT;
   JVal m;
   m.kind = JVal::Obj;
   m.o["format_version"] = jstr("lutkan/1");
@@ -626,6 +620,19 @@ void write_container(const lkg_layer_desc& d, const char* path, int mode) {
   m.o["blobs"] = blobs;
   std::string manifest;
   dump(m, 0, manifest);
+  return manifest;
+}
+
+// save_artifact's container (artifact_io.cpp:206-219 + zip.cpp:80-136) from host arrays.
+// mode: 0 the reference's archive (byte-identical), 1 stored entries, 2 parallel-inflate deflate
+void write_container(const lkg_layer_desc& d, const char* path, int mode) {
+  const bool store = mode == 1;
+  // sizes/offsets at or above `lim` get ZIP64 records; LKG_ZIP64_FORCE=1 (test hook) forces them
+  static const bool force64 = std::getenv("LKG_ZIP64_FORCE") != nullptr;
+  const uint64_t lim = force64 ? 0 : kMax32;
+  const int64_t E = (int64_t)d.in_dim * d.out_dim, K = d.K, Ls = d.L;
+  const bool sr = d.value_repr == LKG_REPR_SPLINE_COMPONENT, f16 = d.param_dtype == LKG_PARAM_F16;
+  const std::string manifest = manifest_text(d);
   // blobs: little-endian (the host byte order on x86-64); f16 params re-encoded (float16.cpp)
   auto enc16 = [](const float* v, int64_t n) {
     std::vector<uint8_t> o((size_t)n * 2);
@@ -1045,6 +1052,19 @@ extern "C" lkg_status lkg_artifact_load(lkg_ctx* ctx, const char* path, lkg_laye
     read_container(path, P, false);
     const lkg_status us = lkg_layer_upload(ctx, &P.d, out);  // finalize checks + device upload + tiles
     if (us != LKG_OK) io_fail(us, lkg_last_error());
+  });
+}
+
+extern "C" lkg_status lkg_artifact_manifest(const lkg_layer_desc* d, char* buf, size_t cap, size_t* len) {
+  return io_guarded([&] {
+    if (!d || !len) io_fail(LKG_ERR_INVALID_ARG, "null argument");
+    const std::string m = manifest_text(*d);  // metadata only: no array is read
+    *len = m.size();
+    if (buf && cap) {
+      const size_t n = std::min(cap - 1, m.size());
+      std::memcpy(buf, m.data(), n);
+      buf[n] = 0;
+    }
   });
 }
 

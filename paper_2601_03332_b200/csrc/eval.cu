@@ -32,7 +32,8 @@ using lkg::f64ref::kMaxP;
 using lkg::f64ref::kMaxT;
 
 struct EvalArgs {
-  const float* X;
+  const void* X;         // f32, or f64 (x_f64: the reference's Matrix values unrounded)
+  int32_t x_f64;
   int64_t rows;
   int32_t d, m, R, p, nT, K, L;
   int32_t half_open, zs, phi, i8, JT, RB;
@@ -73,7 +74,8 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const __grid_constant__ 
     __syncthreads();
     const int i = c0 + jt;
     if (row < a.rows && i < a.d) {
-      const double x = (double)a.X[row * a.d + i];
+      const double x = a.x_f64 ? static_cast<const double*>(a.X)[row * a.d + i]
+                               : (double)static_cast<const float*>(a.X)[row * a.d + i];
       int fl = 0;
       if (!isfinite(x)) nonfinite = true;
       const bool in = a.half_open ? (a.lo <= x && x < a.hi) : (a.lo <= x && x <= a.hi);  // runtime.cpp:71-75
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(kThreads) eval_kernel(const __grid_constant__ 
 
 namespace lkg {
 
-void launch_eval(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const float* X, int64_t rows,
+void launch_eval(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const void* X, bool x_f64, int64_t rows,
                  double* dsum, unsigned long long* u) {
   EvalArgs a{};
   std::vector<double> ext;
@@ -176,6 +178,7 @@ void launch_eval(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const floa
   if (!L->q.p && !L->float_table.p)
     throw Error{LKG_ERR_CONFIG, "eval_accuracy needs the reference-layout table (layer stored tiles-only)"};
   a.X = X;
+  a.x_f64 = x_f64;
   a.rows = rows;
   a.d = S->in_dim;
   a.m = S->col1 - S->col0;

@@ -161,7 +161,7 @@ void launch_edge_phi(lkg_ctx* ctx, const lkg_spec* S, const int32_t* e, const do
                      int* flags);
 void launch_quantize(lkg_ctx* ctx, const double* v, int64_t nseg, int L, int asym, int32_t* q, double* scale,
                      double* ymin, int* flags);  // finalize checks (runtime.cpp:11-43)
-void launch_eval(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const float* X, int64_t rows,
+void launch_eval(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const void* X, bool x_f64, int64_t rows,
                  double* dsum, unsigned long long* u);
 bool launch_spline_tiled(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows, float* Y);
 

@@ -782,6 +782,23 @@ def save_artifact(artifact: "LutLayerArtifact", path, engine: Engine | None = No
     check(lib().lkg_artifact_save(eng.handle, artifact.device(eng).handle, os.fsencode(path), mode))
 
 
+def artifact_manifest_json(artifact: "LutLayerArtifact") -> str:
+    """artifact_io.cpp:98-124 — the manifest text exactly as save_artifact writes it (host only)."""
+    d = _capi.LayerDesc()
+    K = artifact._origin.info.K if artifact._origin is not None else artifact.K  # no table download
+    d.in_dim, d.out_dim, d.K, d.L = artifact.in_dim, artifact.out_dim, K, artifact.L
+    d.value_repr, d.interp, d.scheme = int(artifact.value_repr), 0, int(artifact.scheme)
+    d.dtype, d.param_dtype = int(artifact.dtype), int(artifact.param_dtype)
+    d.boundary_mode, d.oob_policy = int(artifact.oob.boundary_mode), int(artifact.oob.oob_policy)
+    base = (artifact.base_kind or "").encode()
+    d.base_kind = base
+    n = C.c_size_t()
+    check(lib().lkg_artifact_manifest(C.byref(d), None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(lib().lkg_artifact_manifest(C.byref(d), buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
 def check_artifact(path) -> None:
     """Every load_artifact check (artifact_io.cpp:221-300 + finalize) without a device upload;
     raises the reference's error class."""
@@ -873,9 +890,14 @@ def eval_accuracy(layer: KanLayerSpec, artifact: "LutLayerArtifact", X, engine: 
         X = np.asarray(X)
         if X.ndim != 2 or X.shape[1] != layer.in_dim:
             raise DimensionError("input column count does not match in_dim")
-        X = np.ascontiguousarray(X, np.float32)
-        check(lib().lkg_eval_accuracy_host(eng.handle, spec.handle, dl.handle, X.ctypes.data_as(C.c_void_p),
-                                           X.shape[0], C.byref(r)))
+        if X.dtype == np.float64:  # the reference's f64 Matrix values, evaluated unrounded
+            X = np.ascontiguousarray(X)
+            check(lib().lkg_eval_accuracy_host_f64(eng.handle, spec.handle, dl.handle, X.ctypes.data_as(C.c_void_p),
+                                                   X.shape[0], C.byref(r)))
+        else:
+            X = np.ascontiguousarray(X, np.float32)
+            check(lib().lkg_eval_accuracy_host(eng.handle, spec.handle, dl.handle, X.ctypes.data_as(C.c_void_p),
+                                               X.shape[0], C.byref(r)))
     q = QuantConfig(artifact.L, artifact.scheme, artifact.dtype, artifact.value_repr, artifact.interp,
                     artifact.param_dtype)
     return EvalReport(q, artifact.oob, 0, int(r.n_samples), r.mae_inrange, r.maxabs_inrange,
