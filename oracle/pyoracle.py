@@ -123,7 +123,7 @@ def build(ref: bool = True) -> None:
     """Build the port (always) and the in-place reference build (only where /root/reference exists)."""
     targets = ["port"]
     if ref and os.path.isdir("/root/reference/proj/core/src"):
-        targets.append("ref")
+        targets += ["ref", "sweep"]  # sweep: the reference's run_sweep/collect_results (tests/test_sweep.py)
         lib = os.path.join(os.path.dirname(HERE), "paper_2601_03332_b200", "liblutkan_b200.so")
         if os.path.exists(lib):
             targets.append("shim")  # C++ drop-in shim test against the reference library

@@ -232,3 +232,26 @@ def test_gpu_sweep_with_speed_and_failures(lk, sw, tmp_path):
         sw.run_honest_bench(layer, d / "artifact.lut", X, sw.BenchOptions(threads=2))
     with pytest.raises(lk.DimensionError):
         sw.run_honest_bench(layer, d / "artifact.lut", X[:, :4])
+
+
+def test_reference_collect_reads_gpu_sweep_files(sw, tmp_path):
+    """The REFERENCE's run_sweep + collect_results (oracle/_ref/sweep_ref) over a cell written by
+    the GPU sweep (tests/golden/sweep_gpu: configs[2]-shaped L=64 cell from tools/sweeps/c3_grid.json,
+    eval + honest-bench reports): it skips the complete cell, reads our report files, and its CSVs
+    equal ours byte for byte."""
+    import subprocess
+    binp = os.path.join(os.path.dirname(GOLD), "..", "..", "oracle", "_ref", "sweep_ref")
+    if not os.path.exists(binp):
+        pytest.skip("oracle/_ref/sweep_ref not built (make -C oracle ref sweep; needs /root/reference)")
+    root = tmp_path / "root"
+    shutil.copytree(os.path.join(os.path.dirname(GOLD), "sweep_gpu"), root)
+    cfg = tmp_path / "cfg.json"
+    cfg.write_text(json.dumps({"Ls": [64], "schemes": ["symmetric"], "boundary_modes": ["half_open"],
+                               "oob_policies": ["clip_x"], "seeds": [2], "in_dim": 64, "out_dim": 64}))
+    out = subprocess.run([binp, str(cfg), str(root), str(tmp_path / "ref_csv")], check=True, capture_output=True,
+                         text=True).stdout
+    assert json.loads(out) == {"n_total": 1, "n_run": 0, "n_skipped": 1, "n_failed": 0}
+    sw.collect_results(root, tmp_path / "our_csv")
+    for fn in ("accuracy", "oob_matrix", "memory", "speed_scalar", "speed_optimized"):
+        assert (tmp_path / "our_csv" / f"{fn}.csv").read_bytes() == (tmp_path / "ref_csv" / f"{fn}.csv").read_bytes()
+    assert _csv_rows(tmp_path / "our_csv" / "speed_optimized.csv")[1][4] == "1"
