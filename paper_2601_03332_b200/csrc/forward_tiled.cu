@@ -70,6 +70,7 @@ struct TiledArgs {
   lkg::CoordConst cc;        // coordinate constants (coords.cuh)
   int64_t n_items, n_rt;
   int32_t ns;           // stage buffers (2 or 3, whatever fits shared memory)
+  uint32_t rt_group;    // row tiles per item group (item_coords)
   float4 ktab[kMaxKT];  // {T_k, T_k+1, (L-1)/(T_k+1 - T_k), 0}
   // fused next layer (FUSE): a small-out_dim layer evaluated in the epilogue from the 16 hidden
   // activations each lane holds (the whole-layer "small" layout, resident in shared memory)
@@ -91,19 +92,18 @@ __device__ __forceinline__ float magic(uint32_t w, uint32_t sel) {
 }
 
 // Item u -> (row tile, j-block). GC: row tiles fastest (every CTA in flight shares the current
-// tile in L2). Otherwise groups of kRtGroup row tiles sweep all j-blocks with the row tile
+// tile in L2). Otherwise groups of a.rt_group row tiles sweep all j-blocks with the row tile
 // fastest: the group's x blocks stay in L2 across j-blocks and each tile is read once per group
 // (C4: DRAM traffic per layer 17 GB -> ~5 GB).
-constexpr uint32_t kRtGroup = 8;
 __device__ __forceinline__ void item_coords(const TiledArgs& a, bool gc, uint32_t u, uint32_t& rt, int& jb) {
-  const uint32_t n_rt = (uint32_t)a.n_rt, n_jb = (uint32_t)a.n_jb;
+  const uint32_t n_rt = (uint32_t)a.n_rt, n_jb = (uint32_t)a.n_jb, rg = a.rt_group;
   if (gc) {
     rt = u % n_rt;
     jb = (int)(u / n_rt);
     return;
   }
-  const uint32_t per = kRtGroup * n_jb, g = u / per, base = g * kRtGroup;
-  const uint32_t gsz = n_rt - base < kRtGroup ? n_rt - base : kRtGroup, ul = u - g * per;
+  const uint32_t per = rg * n_jb, g = u / per, base = g * rg;
+  const uint32_t gsz = n_rt - base < rg ? n_rt - base : rg, ul = u - g * per;
   rt = base + ul % gsz;
   jb = (int)(ul / gsz);
 }
@@ -1041,6 +1041,11 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   const int grid = (int)std::min<int64_t>(a.n_items, sm_count(ctx->device));
   const size_t extra = (L2 && !gm.codes_global) ? kMaxKT * 16 + ((L2->geom.tile_bytes + 15) & ~15) : 0;
   a.ns = tiled_stages(L, W, R, extra);
+  {  // row tiles per item group (item_coords). Measured on configs[3] layer 1 (1M rows): 4/8/16/32
+     // within 1.5% of each other; L2 evict_last/evict_first hints on x/tiles doubled DRAM reads.
+    static const char* rg = getenv("LKG_RTG");  // tuning hook
+    a.rt_group = rg ? (uint32_t)std::max(1, atoi(rg)) : 8u;
+  }
   size_t smem = tiled_smem(L, W, R, a.ns);
   const int sel = (asym << 2) | (sr << 1) | (int)zs;
   if (gm.codes_global) {
