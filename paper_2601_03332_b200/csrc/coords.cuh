@@ -39,9 +39,9 @@ __device__ __forceinline__ Coord lut_coords(const CoordConst& c, const float4* k
   o.xp = xp;
   int k = min(__float2int_rd((xp - c.lo) * c.inv_h), c.K - 1);
   float4 kt = ktab[k];
-  k = k - (xp < kt.x ? 1 : 0) + ((xp >= kt.y && k < c.K - 1) ? 1 : 0);
+  k = k - (xp < kt.x ? 1 : 0) + ((xp >= kt.z && k < c.K - 1) ? 1 : 0);
   kt = ktab[k];
-  const float dx = xp - kt.x, z = dx * kt.z, fl = floorf(z);
+  const float dx = xp - kt.x, z = dx * kt.y, fl = floorf(z);
   float w1 = z - fl;
   int l0 = (int)fl;
   const bool top = xp == c.hi_clip;
@@ -49,7 +49,7 @@ __device__ __forceinline__ Coord lut_coords(const CoordConst& c, const float4* k
   w1 = top ? c.top_w1 : w1;
   if (!top && dx != 0.0f && (w1 < c.z_thr || w1 > 1.0f - c.z_thr)) {
     // near a sample node: u and z exactly as runtime.cpp:178-181 (f64)
-    const double u = ((double)xp - (double)kt.x) / ((double)kt.y - (double)kt.x);
+    const double u = ((double)xp - (double)kt.x) / ((double)kt.z - (double)kt.x);
     const double zz = u * (double)(c.L - 1);
     int ll = (int)floor(zz);
     ll = ll < 0 ? 0 : (ll > c.L - 1 ? c.L - 1 : ll);
@@ -82,34 +82,41 @@ __device__ __forceinline__ float silu_fast(float x) {
 // Branch-free half of lut_coords_fast: the fast coordinates and whether the exact path must
 // replace them (lets a caller run several rows' coordinate chains side by side and take the
 // exact path once for all of them).
+// floor() of a value in [0, 2^23) on the FMA/ALU pipes: the round-down add leaves 2^23 + floor(v)
+// in the float and floor(v) in its low mantissa bits (no F2I / FRND, which issue at 1/8 rate).
+__device__ __forceinline__ float floor_magic(float v) { return __fadd_rd(v, 8388608.0f); }
+__device__ __forceinline__ int floor_magic_int(float m) { return __float_as_int(m) - 0x4B000000; }
+
 __device__ __forceinline__ Coord lut_coords_fast_nb(const CoordConst& c, const float4* ktab, float x, bool& slow) {
   const float xp = fminf(fmaxf(x, c.lo), c.hi_clip);
-  const int k = min(__float2int_rd((xp - c.lo) * c.inv_h), c.K - 1);
-  const float4 kt = ktab[k];
-  const float dx = xp - kt.x, z1 = fmaf(dx, kt.z, 1.0f), zf = floorf(z1), w1 = z1 - zf;
+  const int k = min(floor_magic_int(floor_magic((xp - c.lo) * c.inv_h)), c.K - 1);
+  const float2 kt = *reinterpret_cast<const float2*>(ktab + k);  // {T_k, (L-1)/h_k}
+  const float dx = xp - kt.x, z1 = fmaf(dx, kt.y, 1.0f), zm = floor_magic(z1), zf = zm - 8388608.0f;
+  const float w1 = z1 - zf;
   const bool top = xp == c.hi_clip;
   slow = !top && dx != 0.0f && fabsf(w1 - 0.5f) > c.fast_half;
   Coord o;
-  o.in = c.lo <= x && x <= c.hi_clip;
+  o.in = xp == x;  // == (t_0 <= x <= hi_clip): clamping changes every other x; NaN compares false
   o.xp = xp;
   o.k = k;
-  o.l0 = top ? c.top_l0 : (int)zf - 1;
+  o.l0 = top ? c.top_l0 : floor_magic_int(zm) - 1;
   o.w1 = top ? c.top_w1 : w1;
   return o;
 }
 
 __device__ __forceinline__ Coord lut_coords_fast(const CoordConst& c, const float4* ktab, float x) {
   const float xp = fminf(fmaxf(x, c.lo), c.hi_clip);
-  const int k = min(__float2int_rd((xp - c.lo) * c.inv_h), c.K - 1);
-  const float4 kt = ktab[k];
-  const float dx = xp - kt.x, z1 = fmaf(dx, kt.z, 1.0f), zf = floorf(z1), w1 = z1 - zf;
+  const int k = min(floor_magic_int(floor_magic((xp - c.lo) * c.inv_h)), c.K - 1);
+  const float2 kt = *reinterpret_cast<const float2*>(ktab + k);  // {T_k, (L-1)/h_k}
+  const float dx = xp - kt.x, z1 = fmaf(dx, kt.y, 1.0f), zm = floor_magic(z1), zf = zm - 8388608.0f;
+  const float w1 = z1 - zf;
   const bool top = xp == c.hi_clip;  // exact host-side coordinates; dx == 0: z = 0 exactly
   if (!top && dx != 0.0f && fabsf(w1 - 0.5f) > c.fast_half) return lut_coords(c, ktab, x);
   Coord o;
   o.in = c.lo <= x && x <= c.hi_clip;
   o.xp = xp;
   o.k = k;
-  o.l0 = top ? c.top_l0 : (int)zf - 1;
+  o.l0 = top ? c.top_l0 : floor_magic_int(zm) - 1;
   o.w1 = top ? c.top_w1 : w1;
   return o;
 }

@@ -71,7 +71,7 @@ struct TiledArgs {
   int64_t n_items, n_rt;
   int32_t ns;           // stage buffers (2 or 3, whatever fits shared memory)
   uint32_t rt_group;    // row tiles per item group (item_coords)
-  float4 ktab[kMaxKT];  // {T_k, T_k+1, (L-1)/(T_k+1 - T_k), 0}
+  float4 ktab[kMaxKT];  // {T_k, (L-1)/(T_k+1 - T_k), T_k+1, 0}
   // fused next layer (FUSE): a small-out_dim layer evaluated in the epilogue from the 16 hidden
   // activations each lane holds (the whole-layer "small" layout, resident in shared memory)
   const uint8_t* lut2;
@@ -887,7 +887,7 @@ void fill_coord_const(const lkg_layer* L, CoordConst& c, float4* ktab) {
   c.inv_h = (float)L->K / (hi - c.lo);
   for (int k = 0; k < L->K; k++) {
     const float t0 = L->knots[k], t1 = L->knots[k + 1];
-    ktab[k] = make_float4(t0, t1, (float)(L->L - 1) / (t1 - t0), 0.f);
+    ktab[k] = make_float4(t0, (float)(L->L - 1) / (t1 - t0), t1, 0.f);  // coords.cuh layout
   }
   // fp32 z = (x' - t_k) * (L-1)/h carries <= 3 roundings: re-evaluate in f64 within 8x that of a node
   c.z_thr = (float)std::max(8.0 * 0x1p-24 * (L->L - 1), 0x1p-20);
