@@ -529,6 +529,27 @@ struct SmallArgs {
   float4 ktab[kMaxKT];
 };
 
+// n consecutive floats from shared memory with the widest aligned vector loads
+template <int N>
+__device__ __forceinline__ void lkg_small_load(const float* p, float (&v)[N]) {
+  if constexpr (N % 4 == 0) {
+#pragma unroll
+    for (int j = 0; j < N; j += 4) {
+      const float4 t = *reinterpret_cast<const float4*>(p + j);
+      v[j] = t.x, v[j + 1] = t.y, v[j + 2] = t.z, v[j + 3] = t.w;
+    }
+  } else if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int j = 0; j < N; j += 2) {
+      const float2 t = *reinterpret_cast<const float2*>(p + j);
+      v[j] = t.x, v[j + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; j++) v[j] = p[j];
+  }
+}
+
 template <bool ASYM, bool SR, bool ZS, bool VT, int MPT>
 __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -569,18 +590,23 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
         const float xb = ZS ? x : co.xp;  // clip_x clips the base branch too (runtime.cpp:189)
         bx = lkg::silu_fast(xb);
       }
-      const int cell = i * K + co.k, l1 = min(co.l0 + 1, L - 1);
+      const int cell = i * K + co.k;
       const float w1 = co.w1, w0 = 1.0f - w1;
       const float* CB = CBt + i * MP;
       if (VT) {
+        // V1 is the next line: l0 = L-1 comes with w1 = 0, and the table ends with a padding line
         const float* V0 = V + (cell * L + co.l0) * MPT;
-        const float* V1 = V + (cell * L + l1) * MPT;
+        float v0[MPT], v1[MPT], cb[MPT];
+        lkg_small_load<MPT>(V0, v0);
+        lkg_small_load<MPT>(V0 + MPT, v1);
+        if (SR) lkg_small_load<MPT>(CB, cb);
 #pragma unroll
         for (int j = 0; j < MPT; j++) {
-          const float v = tab ? fmaf(w1, V1[j], w0 * V0[j]) : 0.0f;
-          y[j] += SR ? fmaf(CB[j], bx, v) : v;
+          const float v = tab ? fmaf(w1, v1[j], w0 * v0[j]) : 0.0f;
+          y[j] += SR ? fmaf(cb[j], bx, v) : v;
         }
       } else {
+        const int l1 = min(co.l0 + 1, L - 1);
         const uint8_t* c0 = lut + (cell * L + co.l0) * MP;
         const uint8_t* c1 = lut + (cell * L + l1) * MP;
         const float* P = reinterpret_cast<const float*>(lut + a.p_off) + cell * MP;
@@ -600,20 +626,25 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
         }
       }
     };
-    auto x_at = [&](int i) -> int64_t {
-      if (a.x_blk > 0) {
+    const float* xrow = a.X + row * x_rs;  // this row (row-major layout)
+    auto x_ptr = [&](int i) -> const float* {
+      if (a.x_blk > 0) {  // blocked all-gather layout [i / x_blk][rows][x_blk]
         const int b = i / a.x_blk;
-        return (int64_t)b * a.rows * a.x_blk + row * x_rs + (i - b * a.x_blk);
+        return a.X + (int64_t)b * a.rows * a.x_blk + row * x_rs + (i - b * a.x_blk);
       }
-      return row * x_rs + i;
+      return xrow + i;
     };
     if (pairs) {
       // inputs in pairs (i even): one 8-byte load, both fast coordinate chains side by side,
       // the exact path once if either needs it
+      // the next pair's load is issued one iteration ahead (its latency was the top stall)
       int i = 2 * (lane % (d >> 1));
+      float2 xn = make_float2(lo, lo);
+      if (vrow) xn = __ldg(reinterpret_cast<const float2*>(x_ptr(i)));
       for (int t = 0; t < d; t += 2, i = (i + 2 == d) ? 0 : i + 2) {
-        float2 xx = make_float2(lo, lo);
-        if (vrow) xx = __ldg(reinterpret_cast<const float2*>(a.X + x_at(i)));
+        const float2 xx = xn;
+        const int inx = (i + 2 == d) ? 0 : i + 2;
+        if (vrow && t + 2 < d) xn = __ldg(reinterpret_cast<const float2*>(x_ptr(inx)));
         bool s0, s1;
         lkg::Coord c0 = lkg::lut_coords_fast_nb(a.cc, ktab, xx.x, s0);
         lkg::Coord c1 = lkg::lut_coords_fast_nb(a.cc, ktab, xx.y, s1);
@@ -627,9 +658,11 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
       }
     } else {
       int i = i0;
+      float xn = lo;
+      if (vrow) xn = __ldg(x_ptr(i));
       for (int t = 0; t < d; t++, i = (i + 1 == d) ? 0 : i + 1) {
-        float x = lo;
-        if (vrow) x = __ldg(a.X + x_at(i));
+        const float x = xn;
+        if (vrow && t + 1 < d) xn = __ldg(x_ptr(i + 1 == d ? 0 : i + 1));
         const lkg::Coord co = lkg::lut_coords_fast(a.cc, ktab, x);
         nfacc = fmaf(x, 0.0f, nfacc);
         accum(i, x, co);
@@ -764,7 +797,7 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
     const int MP = m <= 1 ? 1 : (m <= 2 ? 2 : (m <= 4 ? 4 : 8));
     // preferred: dequantized value table V = out*spline*(y_min + scale*q) in f32 (one rounding of
     // the f64 product), so the table walk is two loads and two FMAs per edge
-    const int64_t vt = ((int64_t)d * K * Ls * MP * 4 + 15) / 16 * 16;
+    const int64_t vt = ((int64_t)(d * K * Ls + 1) * MP * 4 + 15) / 16 * 16;  // + one padding line
     const int64_t vt_total = vt + ((int64_t)d * MP * 4 + 15) / 16 * 16;
     if (vt_total + kMaxKT * 16 <= kSmallMaxBytes) {
       gm.small = 2;
