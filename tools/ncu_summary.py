@@ -15,7 +15,8 @@ METRICS = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "smsp__issue_act
            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
            "l1tex__throughput.avg.pct_of_peak_sustained_active", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
            "smsp__warps_eligible.avg.per_cycle_active", "launch__registers_per_thread",
-           "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
+           "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]
 STALLS = ["stall_math", "stall_wait", "stall_dispatch", "stall_short_sb", "stall_not_selected", "stall_selected",
           "stall_lg", "stall_barrier", "stall_long_sb", "stall_mio", "stall_branch_resolving", "stall_no_inst",
           "stall_sleep", "stall_misc", "stall_membar", "stall_drain", "stall_tex"]
