@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       const uint8_t* T = stage + (g % NS) * sb - so;  // T + p_off is the staged P block
       const uint8_t* Tcodes = GC ? a.tiles + ((int64_t)jb * a.n_ih + ih) * tb : T;
 
+      // one step per iteration: unrolling by 2 spills 64 B and measured -5% (C2), -7% (C2a)
 #pragma unroll 1
       for (int s = 0; s < G; s++) {
         const int il = (s + lane) & 7;
