@@ -172,12 +172,19 @@ def sample_rows_for(ee_row, nthreads, rows, seconds=3.0):
 
 
 def cpu_baseline(wl):
+    """The reference's lut_model_forward_batch on the box's host cores (all threads, rows sharded),
+    plus the reference's own single-thread protocol figure (bench.hpp:14-15: one thread) and its
+    compile_layer time for the same chain."""
     from oracle.pyoracle import Oracle
     cfg, rows, L, scheme, bm, op = WORKLOADS[wl]
     o = Oracle("auto")
     dims = o_dims(cfg)
-    chain = [o.compile_layer(o.recipe_layer(cfg, l), L, scheme, 1, 0, bm, op) for l in range(len(dims) - 1)]
-    ee_row = sum(dims[l] * dims[l + 1] for l in range(len(dims) - 1))
+    nl = len(dims) - 1
+    specs = [o.recipe_layer(cfg, l) for l in range(nl)]
+    t0 = time.perf_counter()
+    chain = [o.compile_layer(specs[l], L, scheme, 1, 0, bm, op) for l in range(nl)]
+    compile_s = time.perf_counter() - t0
+    ee_row = sum(dims[l] * dims[l + 1] for l in range(nl))
     nthreads = os.cpu_count() or 1
     n = sample_rows_for(ee_row, nthreads, rows, seconds=10.0)
     X = o.recipe_inputs(cfg, 0, n).astype(np.float64)
@@ -185,8 +192,16 @@ def cpu_baseline(wl):
     t0 = time.perf_counter()
     o.lut_model_forward(chain, X, 1, nthreads)
     sec = time.perf_counter() - t0
+    n1 = sample_rows_for(ee_row, 1, rows, seconds=3.0)
+    o.lut_model_forward(chain, X[: max(1, n1 // 20)], 1, 1)
+    t0 = time.perf_counter()
+    o.lut_model_forward(chain, X[:n1], 1, 1)
+    sec1 = time.perf_counter() - t0
     return {"value": n * ee_row / sec, "unit": "edge-evals/s", "cores": nthreads, "kind": o.kind,
-            "sample": f"{n} rows of {wl} (reference lut_model_forward_batch, Tier::Optimized, {nthreads} threads)"}
+            "sample": f"{n} rows of {wl} (reference lut_model_forward_batch, Tier::Optimized, {nthreads} threads)",
+            "single_thread": {"value": n1 * ee_row / sec1, "unit": "edge-evals/s", "cores": 1,
+                              "sample": f"{n1} rows, one thread (the reference's timing protocol)"},
+            "compile_s": compile_s, "compile_note": f"reference compile_layer of the {nl}-layer chain, one thread"}
 
 
 def run_c5(args):
