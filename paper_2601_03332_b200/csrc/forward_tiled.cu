@@ -154,13 +154,28 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   const uint32_t tm_base = F64 ? *tm_base_s : 0u;
   const uint32_t tm_warp = tm_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * R * 32);
 
-  const int64_t n_local = a.n_items > blockIdx.x ? (a.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // Balanced rows (one j-block, e.g. configs[1] layer 0): CTA b owns rows [r_lo, r_hi) of an equal
+  // split (starts at multiples of 64 rows, so every row keeps its lane and rotation and its result
+  // bits), walked in 1024-row tiles; the warps past r_hi in the last tile only keep the stage
+  // protocol. Whole 1024-row items over 148 CTAs would leave 6.6 items per CTA waiting on 7.
+  constexpr int64_t TILE_ROWS = W * ROWS_W;
+  const bool bal = a.n_jb == 1 && !GC;
+  int64_t r_lo = 0, r_hi = a.rows;
+  if (bal) {
+    auto split = [&](int64_t b) -> int64_t {
+      return b >= (int64_t)gridDim.x ? a.rows : (a.rows * b / (int64_t)gridDim.x) / 64 * 64;
+    };
+    r_lo = split(blockIdx.x);
+    r_hi = split((int64_t)blockIdx.x + 1);
+  }
+  const int64_t n_local = bal ? (r_hi - r_lo + TILE_ROWS - 1) / TILE_ROWS
+                              : (a.n_items > blockIdx.x ? (a.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0);
   const int64_t n_stages = n_local * a.n_ih;
   auto issue = [&](int64_t g) {
     const uint32_t gs = (uint32_t)g, item = blockIdx.x + (gs / (uint32_t)a.n_ih) * gridDim.x;
-    uint32_t rt_;
-    int jb;
-    item_coords(a, GC, item, rt_, jb);
+    uint32_t rt_ = 0;
+    int jb = 0;  // balanced rows: the only j-block (local item numbers are not global item ids)
+    if (!bal) item_coords(a, GC, item, rt_, jb);
     const int ih = (int)(gs % (uint32_t)a.n_ih);
     const uint8_t* src = a.tiles + ((int64_t)jb * a.n_ih + ih) * tb + so;
     uint8_t* dst = stage + (g % NS) * sb;
@@ -188,6 +203,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   // t_0: finite and in range, so they never count as OOB; their P and CB entries are 0.
   // Row tile of local item li (32-bit division: item counts are far below 2^31).
   auto row0_of = [&](int64_t li_) -> int64_t {
+    if (bal) return r_lo + li_ * TILE_ROWS + warp * ROWS_W;
     const uint32_t item_ = (uint32_t)(blockIdx.x + li_ * gridDim.x);
     uint32_t rt_;
     int jb_;
@@ -204,13 +220,13 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
     }
     const float* src = a.X + col_ + (r0_ + (lane >> 3)) * x_rs;
     const uint32_t sd = lkg::smem_u32(dst);
-    if (ih_ * G + G <= a.d && r0_ + ROWS_W <= a.rows) {  // whole tile inside X
+    if (ih_ * G + G <= a.d && r0_ + ROWS_W <= r_hi) {  // whole tile inside X (and this CTA's rows)
 #pragma unroll
       for (int t = 0; t < NXL; t++)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sd + 16 * t), "l"(src + (int64_t)(4 * t) * x_rs)
                      : "memory");
     } else {
-      const int64_t left = a.rows - r0_ - (lane >> 3);
+      const int64_t left = r_hi - r0_ - (lane >> 3);
       const bool cin = i_ < a.d;
 #pragma unroll
       for (int t = 0; t < NXL; t++) {
@@ -229,14 +245,15 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
 
   for (int64_t li = 0; li < n_local; li++) {
     const uint32_t item = (uint32_t)(blockIdx.x + li * gridDim.x);
-    uint32_t rt32;
-    int jb;
-    item_coords(a, GC, item, rt32, jb);
+    uint32_t rt32 = 0;
+    int jb = 0;
+    if (!bal) item_coords(a, GC, item, rt32, jb);
     const int64_t rt = rt32;
     const int64_t row0_next = li + 1 < n_local ? row0_of(li + 1) : 0;
     const int cnt = jb == 0;  // OOB statistics are counted once per row (j-block 0)
-    const int64_t row0 = rt * (int64_t)(W * ROWS_W) + warp * ROWS_W;
-    const int64_t rows_left = a.rows - row0;  // rows of this warp: [0, min(ROWS_W, rows_left))
+    const int64_t row0 = bal ? row0_of(li) : rt * TILE_ROWS + warp * ROWS_W;
+    const int64_t rows_left = r_hi - row0;  // rows of this warp: [0, min(ROWS_W, rows_left))
+    const bool wactive = rows_left > 0;     // else: a balanced CTA's last tile past its rows
     float2 acc[R][8];
     uint32_t row_oob = 0;   // bit r: row lane + 32 r saw an OOB coordinate
     uint32_t oob_item = 0;  // OOB coordinates of this lane's rows in this item
@@ -265,8 +282,9 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       const uint8_t* Tcodes = GC ? a.tiles + ((int64_t)jb * a.n_ih + ih) * tb : T;
 
       // one step per iteration: unrolling by 2 spills 64 B and measured -5% (C2), -7% (C2a)
+      const int n_steps = wactive ? G : 0;
 #pragma unroll 1
-      for (int s = 0; s < G; s++) {
+      for (int s = 0; s < n_steps; s++) {
         const int il = (s + lane) & 7;
         const uint8_t* Tq = Tcodes + il * JB;
         const uint8_t* Tp = T + a.p_off + il * PROW;
