@@ -591,10 +591,15 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
   // input pairs need 8-byte aligned (i, i+1) in the same row / column block
   const bool pairs = (d % 2 == 0) && (a.x_blk > 0 ? a.x_blk % 2 == 0 : true) &&
                      ((reinterpret_cast<uintptr_t>(a.X) & 7) == 0);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t rb = (int64_t)blockIdx.x * blockDim.x; rb < a.rows; rb += stride) {
+  // Each block owns an equal, 64-aligned row range (a row keeps its lane, hence its input
+  // rotation and result bits, under any split): the SMs get equal work, where a grid-stride walk
+  // over 1024-row chunks left some SMs 8 chunks and others 6 (configs[1] layer 1).
+  const int64_t b_lo = (a.rows * blockIdx.x / gridDim.x) / 64 * 64;
+  const int64_t b_hi = blockIdx.x + 1 == gridDim.x ? a.rows : (a.rows * (blockIdx.x + 1) / gridDim.x) / 64 * 64;
+  for (int64_t rb = b_lo; rb < b_hi; rb += blockDim.x) {
     const int64_t row = rb + tid;
-    const bool vrow = row < a.rows;
+    if (rb + (tid & ~31) >= b_hi) break;  // this warp has no row left (warp-uniform)
+    const bool vrow = row < b_hi;
     float y[8];
 #pragma unroll
     for (int j = 0; j < 8; j++) y[j] = 0.0f;
@@ -1004,8 +1009,8 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
   a.m = L->col1 - L->col0;
   a.counters = ctx->counters.as<unsigned long long>() + 4 * slot;
   fill_coord_const(L, a.cc, a.ktab);
-  const int blocks_per_sm = gm.tile_bytes <= 100 * 1024 ? 2 : 1;
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 1023) / 1024, blocks_per_sm * sm_count(ctx->device)));
+  // one resident block per SM (1024 threads x ~47 registers) and one equal row range per block
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 1023) / 1024, sm_count(ctx->device)));
   const size_t smem = ((gm.tile_bytes + 15) & ~15) + kMaxKT * 16;
   const bool asym = L->scheme == LKG_SCHEME_ASYMMETRIC, sr = L->value_repr == LKG_REPR_SPLINE_COMPONENT;
   const bool zs = L->oob_policy == LKG_OOB_ZERO_SPLINE;
