@@ -55,7 +55,20 @@ __global__ void __launch_bounds__(W * 32, 1) spline_tiled(const __grid_constant_
     lkg::mbar_fence_init();
   }
   __syncthreads();
-  const int64_t n_local = a.n_items > blockIdx.x ? (a.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  // Balanced rows for one-j-block layers, as the LUT table walk (forward_tiled.cu): CTA b owns an
+  // equal, 64-aligned row range walked in W*ROWS_W-row tiles.
+  constexpr int64_t TILE_ROWS = W * ROWS_W;
+  const bool bal = a.n_jb == 1;
+  int64_t r_lo = 0, r_hi = a.rows;
+  if (bal) {
+    auto split = [&](int64_t b) -> int64_t {
+      return b >= (int64_t)gridDim.x ? a.rows : (a.rows * b / (int64_t)gridDim.x) / 64 * 64;
+    };
+    r_lo = split(blockIdx.x);
+    r_hi = split((int64_t)blockIdx.x + 1);
+  }
+  const int64_t n_local = bal ? (r_hi - r_lo + TILE_ROWS - 1) / TILE_ROWS
+                              : (a.n_items > blockIdx.x ? (a.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0);
   const int64_t n_stages = n_local * a.n_ih;
   auto issue = [&](int64_t g) {
     const int64_t item = blockIdx.x + (g / a.n_ih) * gridDim.x;
@@ -69,9 +82,9 @@ __global__ void __launch_bounds__(W * 32, 1) spline_tiled(const __grid_constant_
   for (int64_t li = 0; li < n_local; li++) {
     const int64_t item = blockIdx.x + li * gridDim.x;
     const int64_t rt = item / a.n_jb;
-    const int jb = (int)(item % a.n_jb);
-    const int64_t row0 = rt * (int64_t)(W * ROWS_W) + warp * ROWS_W;
-    const int64_t rows_left = a.rows - row0;
+    const int jb = bal ? 0 : (int)(item % a.n_jb);
+    const int64_t row0 = bal ? r_lo + li * TILE_ROWS + warp * ROWS_W : rt * TILE_ROWS + warp * ROWS_W;
+    const int64_t rows_left = r_hi - row0;
     float2 acc[RR][8];
     double acc64[F64 ? RR : 1][F64 ? 16 : 1];
 #pragma unroll
