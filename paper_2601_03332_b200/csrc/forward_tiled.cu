@@ -108,7 +108,8 @@ __device__ __forceinline__ void item_coords(const TiledArgs& a, bool gc, uint32_
   jb = (int)(ul / gsz);
 }
 
-template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1, bool GC = false>
+template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1, bool GC = false,
+          bool BAL = false>
 __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int NS = a.ns;
@@ -159,7 +160,8 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   // bits), walked in 1024-row tiles; the warps past r_hi in the last tile only keep the stage
   // protocol. Whole 1024-row items over 148 CTAs would leave 6.6 items per CTA waiting on 7.
   constexpr int64_t TILE_ROWS = W * ROWS_W;
-  const bool bal = a.n_jb == 1 && !GC;
+  // (a compile-time mode: the row-range bookkeeping measured 6.5% on configs[3] layers even when off)
+  constexpr bool bal = BAL;  // launched only for one-j-block, codes-in-smem layers
   int64_t r_lo = 0, r_hi = a.rows;
   if (bal) {
     auto split = [&](int64_t b) -> int64_t {
@@ -777,9 +779,10 @@ __global__ void build_tiles_kernel(const uint8_t* q, const float* scale, const f
     *reinterpret_cast<float*>(t + cb_off + il * PROW + jl * 4) = (float)((double)gains[2 * E + e] * (double)gains[e]);
 }
 
-template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1, bool GC = false>
+template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1, bool GC = false,
+          bool BAL = false>
 void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
-  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC>;
+  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL>;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -1136,7 +1139,7 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
     smem += kMaxKT * 16 + ((g2.tile_bytes + 15) & ~15);
     switch (sel) {
 #define CASE(S) \
-  case S: launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, true>(ctx->stream, a, smem, grid); break;
+  case S: launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, true, 1, false, true>(ctx->stream, a, smem, grid); break;
       CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
     }
@@ -1144,13 +1147,17 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
     ctx->launches++;
     return;
   }
+  const bool bal = !f64 && gm.n_jb == 1;  // balanced rows (fwd_tiled BAL)
   switch (sel) {
-#define CASE(S)                                                                                     \
-  case S:                                                                                           \
-    if (f64)                                                                                        \
-      launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true>(ctx->stream, a, smem, grid); \
-    else                                                                                            \
-      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false>(ctx->stream, a, smem, grid);    \
+#define CASE(S)                                                                                         \
+  case S:                                                                                               \
+    if (f64)                                                                                            \
+      launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true>(ctx->stream, a, smem, grid);     \
+    else if (bal)                                                                                       \
+      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, true>(ctx->stream, a, \
+                                                                                         smem, grid);  \
+    else                                                                                                \
+      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false>(ctx->stream, a, smem, grid);        \
     break;
     CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
