@@ -112,7 +112,10 @@ template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MI
           bool BAL = false>
 __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const int NS = a.ns;
+  // Two stage buffers, a compile-time count: NS as a runtime value (a.ns) turned every per-tile
+  // g mod NS into a 64-bit division (configs[1] layer 0: 0.567 -> 0.534 ms once removed), and more
+  // buffers measured no faster (3: -9% with the runtime count, 4: equal).
+  constexpr int NS = 2;
   constexpr int ROWS_W = 32 * R;        // rows per warp
   constexpr int XS = ROWS_W + 4;        // padded row stride of the transposed x tile
   constexpr int NXL = ROWS_W / 4;        // x elements each lane stages per tile (cp.async)
@@ -173,22 +176,22 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   const int64_t n_local = bal ? (r_hi - r_lo + TILE_ROWS - 1) / TILE_ROWS
                               : (a.n_items > blockIdx.x ? (a.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0);
   const int64_t n_stages = n_local * a.n_ih;
-  auto issue = [&](int64_t g) {
+  auto issue = [&](int64_t g, int st) {  // stage g into buffer st = g mod NS
     const uint32_t gs = (uint32_t)g, item = blockIdx.x + (gs / (uint32_t)a.n_ih) * gridDim.x;
     uint32_t rt_ = 0;
     int jb = 0;  // balanced rows: the only j-block (local item numbers are not global item ids)
     if (!bal) item_coords(a, GC, item, rt_, jb);
     const int ih = (int)(gs % (uint32_t)a.n_ih);
     const uint8_t* src = a.tiles + ((int64_t)jb * a.n_ih + ih) * tb + so;
-    uint8_t* dst = stage + (g % NS) * sb;
-    mbar_expect_tx(&full[g % NS], (uint32_t)sb);
+    uint8_t* dst = stage + st * sb;
+    mbar_expect_tx(&full[st], (uint32_t)sb);
     for (int64_t off = 0; off < sb; off += 32768) {
       const uint32_t n = (uint32_t)(sb - off < 32768 ? sb - off : 32768);
-      bulk_g2s(dst + off, src + off, n, &full[g % NS]);
+      bulk_g2s(dst + off, src + off, n, &full[st]);
     }
   };
   if (tid == 0)
-    for (int64_t g = 0; g < NS && g < n_stages; g++) issue(g);
+    for (int g0 = 0; g0 < NS && g0 < n_stages; g0++) issue(g0, g0);
 
   const float M = 8388608.0f;  // 2^23
   const float OFF = ASYM ? 0.0f : 128.0f;
@@ -279,8 +282,9 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       else if (li + 1 < n_local)
         stage_x(row0_next, 0, xbuf ^ 1);
       xbuf ^= 1;
-      mbar_wait(&full[g % NS], (uint32_t)((g / NS) & 1));
-      const uint8_t* T = stage + (g % NS) * sb - so;  // T + p_off is the staged P block
+      const int st = (int)(g & (NS - 1));
+      mbar_wait(&full[st], (uint32_t)((g / NS) & 1));
+      const uint8_t* T = stage + st * sb - so;  // T + p_off is the staged P block
       const uint8_t* Tcodes = GC ? a.tiles + ((int64_t)jb * a.n_ih + ih) * tb : T;
 
       // one step per iteration: unrolling by 2 spills 64 B and measured -5% (C2), -7% (C2a)
@@ -401,13 +405,12 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       // warps drift up to NS-1 stages apart instead of re-aligning at every tile.
       __syncwarp();
       if (lane == 0) {
-        const int st = (int)(g % NS);
         __threadfence_block();
         if (atomicAdd(&fin[st], 1u) == (uint32_t)(W - 1)) {
           fin[st] = 0;
           __threadfence_block();
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          if (g + NS < n_stages) issue(g + NS);
+          if (g + NS < n_stages) issue(g + NS, st);
         }
       }
     }
@@ -1044,13 +1047,7 @@ static size_t tiled_smem(const lkg_layer* L, int W, int R, int ns = 2) {
   return ns * sb + (size_t)2 * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 64;
 }
 
-// Two stage buffers. Measured on B200 with the barrier-free stage release: a third buffer (where
-// it fits) costs 11% on configs[1] layer 0 (0.652 vs 0.588 ms) and gains nothing elsewhere.
-static int tiled_stages(const lkg_layer* L, int W, int R, size_t extra) {
-  static const char* e = getenv("LKG_STAGES");  // tuning hook: LKG_STAGES=3
-  if (e && e[0] == '3' && tiled_smem(L, W, R, 3) + extra <= 227 * 1024) return 3;
-  return 2;
-}
+static int tiled_stages(const lkg_layer*, int, int, size_t) { return 2; }  // fwd_tiled's NS
 
 bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
   // Off by default: measured on C2, the fused epilogue (16 coordinates per row at the end of
