@@ -113,9 +113,12 @@ template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MI
 __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   // Two stage buffers, a compile-time count: NS as a runtime value (a.ns) turned every per-tile
-  // g mod NS into a 64-bit division (configs[1] layer 0: 0.567 -> 0.534 ms once removed), and more
-  // buffers measured no faster (3: -9% with the runtime count, 4: equal).
-  constexpr int NS = 2;
+  // g mod NS into a 64-bit division (configs[1] layer 0: 0.567 -> 0.534 ms once removed). Three
+  // (LKG_NS=3, the most that fits next to the x tiles) measured 8.5% slower on configs[1].
+#ifndef LKG_NS
+#define LKG_NS 2
+#endif
+  constexpr int NS = LKG_NS;
   constexpr int ROWS_W = 32 * R;        // rows per warp
   constexpr int XS = ROWS_W + 4;        // padded row stride of the transposed x tile
   constexpr int NXL = ROWS_W / 4;        // x elements each lane stages per tile (cp.async)
@@ -282,8 +285,8 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       else if (li + 1 < n_local)
         stage_x(row0_next, 0, xbuf ^ 1);
       xbuf ^= 1;
-      const int st = (int)(g & (NS - 1));
-      mbar_wait(&full[st], (uint32_t)((g / NS) & 1));
+      const int st = (int)((uint32_t)g % NS);  // constant divisor: multiply-shift
+      mbar_wait(&full[st], ((uint32_t)g / NS) & 1u);
       const uint8_t* T = stage + st * sb - so;  // T + p_off is the staged P block
       const uint8_t* Tcodes = GC ? a.tiles + ((int64_t)jb * a.n_ih + ih) * tb : T;
 
@@ -1047,7 +1050,7 @@ static size_t tiled_smem(const lkg_layer* L, int W, int R, int ns = 2) {
   return ns * sb + (size_t)2 * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 64;
 }
 
-static int tiled_stages(const lkg_layer*, int, int, size_t) { return 2; }  // fwd_tiled's NS
+static int tiled_stages(const lkg_layer*, int, int, size_t) { return LKG_NS; }  // fwd_tiled's NS
 
 bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
   // Off by default: measured on C2, the fused epilogue (16 coordinates per row at the end of

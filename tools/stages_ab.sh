@@ -1,9 +1,10 @@
-# A/B of the in-tree build against ab/liblutkan_base.so on the main layer shapes
+# A/B of the in-tree build against other ab/ builds on the C2 layer shapes
+libs=${1:-"default base"}
 for rep in 1 2; do
-  for wl in c2:0 c3:0 c2a:0; do
-    echo -n "[default] "; timeout 300 python tools/time_layer.py ${wl%%:*} ${wl##*:} 50 2>&1 | tail -1
-    echo -n "[base] "; LKG_LIB=$PWD/ab/liblutkan_base.so timeout 300 python tools/time_layer.py ${wl%%:*} ${wl##*:} 50 2>&1 | tail -1
+  for wl in c2:0 c2a:0; do
+    for l in $libs; do
+      if [ "$l" = default ]; then unset LKG_LIB; else export LKG_LIB=$PWD/ab/liblutkan_$l.so; fi
+      echo -n "[$l] "; timeout 300 python tools/time_layer.py ${wl%%:*} ${wl##*:} 50 2>&1 | tail -1
+    done
   done
 done
-echo -n "[default] "; timeout 300 python tools/time_layer.py c4 1 3 2>&1 | tail -1
-echo -n "[base] "; LKG_LIB=$PWD/ab/liblutkan_base.so timeout 300 python tools/time_layer.py c4 1 3 2>&1 | tail -1
