@@ -233,10 +233,12 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
     const float* src = a.X + col_ + (r0_ + (lane >> 3)) * x_rs;
     const uint32_t sd = lkg::smem_u32(dst);
     if (ih_ * G + G <= a.d && r0_ + ROWS_W <= r_hi) {  // whole tile inside X (and this CTA's rows)
+      // one running byte address (a 64-bit add per copy instead of an index-to-address chain)
+      const uint64_t step = (uint64_t)(4 * x_rs) * sizeof(float);
+      uint64_t pa = reinterpret_cast<uint64_t>(src);
 #pragma unroll
-      for (int t = 0; t < NXL; t++)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sd + 16 * t), "l"(src + (int64_t)(4 * t) * x_rs)
-                     : "memory");
+      for (int t = 0; t < NXL; t++, pa += step)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sd + 16 * t), "l"(pa) : "memory");
     } else {
       const int64_t left = r_hi - r0_ - (lane >> 3);
       const bool cin = i_ < a.d;
