@@ -180,6 +180,17 @@ lkg_status lkg_model_forward(lkg_ctx* ctx, const lkg_layer* const* chain, int32_
 lkg_status lkg_model_forward_host(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n_layers,
                                   const float* X_host, int64_t rows, float* Y_host,
                                   lkg_oob_stats* stats);
+/* A chain forward captured once as a CUDA graph and replayed: the same launches as
+ * lkg_model_forward on the same DEVICE buffers (X, Y and the layers are bound at capture; rows > 0),
+ * one cudaGraphLaunch per replay on ctx's stream, asynchronous. For small, latency-bound batches
+ * served repeatedly. Creation runs the chain once eagerly (sizes scratch, sets kernel attributes).
+ * OOB statistics of the replays accumulate in ctx like direct calls (lkg_ctx_collect). The layers,
+ * X and Y must outlive the graph. */
+typedef struct lkg_graph lkg_graph;
+lkg_status lkg_graph_create(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n_layers, const float* X,
+                            int64_t rows, float* Y, lkg_graph** out);
+lkg_status lkg_graph_launch(lkg_graph* graph);
+lkg_status lkg_graph_destroy(lkg_graph* graph);
 /* Per-element coordinates exactly as the forward kernels compute them (steps 1-4 of the
  * 5-step pipeline, runtime.cpp:45-75 / 170-190): for x [n] fp32 (device), writes
  * in-range mask, segment index k and sample index l0 (device int32 arrays, any may be NULL).

@@ -5,7 +5,7 @@ forward and the same-backend B-spline forward, executed by hand-written sm_100a
 CUDA kernels in ``liblutkan_b200.so`` behind the C-ABI ``include/lutkan_b200.h``.
 """
 from .lutkan import (  # noqa: F401
-    BoundaryMode, ChainBatchResult, ConfigError, CudaError, DimensionError, Dtype, Engine, Error, EvalReport,
+    BoundaryMode, ChainBatchResult, ChainGraph, ConfigError, CudaError, DimensionError, Dtype, Engine, Error, EvalReport,
     Interp, KanLayerSpec, MemoryBreakdown, eval_accuracy, memory_breakdown, IoError, CorruptArchiveError,
     CorruptBlobError, MissingKeyError, ShapeError, VersionError, EnumError, save_artifact, load_artifact, check_artifact, artifact_manifest_json, lut_coords, in_range,
     lut_eval_value, lut_eval_phi, basis_values, eval_spline, base_fn, eval_edge_phi, layer_forward,

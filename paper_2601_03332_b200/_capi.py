@@ -97,6 +97,10 @@ SIGNATURES = {
     "lkg_artifact_load": (C.c_int, [C.c_void_p, C.c_char_p, _P(C.c_void_p)]),
     "lkg_artifact_save_desc": (C.c_int, [_P(LayerDesc), C.c_char_p, C.c_int32]),
     "lkg_artifact_check": (C.c_int, [C.c_char_p]),
+    "lkg_graph_create": (C.c_int, [C.c_void_p, _P(C.c_void_p), C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
+                                   _P(C.c_void_p)]),
+    "lkg_graph_launch": (C.c_int, [C.c_void_p]),
+    "lkg_graph_destroy": (C.c_int, [C.c_void_p]),
     "lkg_artifact_manifest": (C.c_int, [_P(LayerDesc), C.c_char_p, C.c_size_t, _P(C.c_size_t)]),
     "lkg_lut_coords64": (C.c_int, [C.c_void_p, C.c_void_p, f64p, C.c_int64, u8p, f64p, i32p, i32p, i32p, f64p]),
     "lkg_lut_eval": (C.c_int, [C.c_void_p, C.c_void_p, i32p, f64p, C.c_int64, f64p, u8p, f64p]),

@@ -635,6 +635,81 @@ lkg_status lkg_model_forward(lkg_ctx* ctx, const lkg_layer* const* chain, int32_
   });
 }
 
+// ---------------------------------------------------------------- CUDA graph of a chain forward
+struct lkg_graph {
+  lkg_ctx* ctx = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int32_t n = 0;
+  int64_t rows = 0;
+  uint64_t kernels = 0;          // launches per replay
+  std::vector<int32_t> in_dims;  // per layer slot (OobStats bookkeeping of each replay)
+};
+
+lkg_status lkg_graph_create(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n, const float* X, int64_t rows,
+                            float* Y, lkg_graph** out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    *out = nullptr;
+    check_chain(chain, n);
+    if (rows <= 0) fail(LKG_ERR_DIMENSION, "a captured forward needs at least one row");
+    need(X, "X");
+    need(Y, "Y");
+    DeviceGuard g(ctx->device);
+    // one eager pass first: scratch buffers sized, kernel attributes set (neither is a stream
+    // operation a capture could record), and the chain validated
+    run_chain(ctx, chain, n, X, rows, Y);
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    reset_slots(ctx, n);
+    for (int s = 0; s < n; s++) ctx->rows_seen[s] = 0;
+    auto G = std::make_unique<lkg_graph>();
+    G->ctx = ctx;
+    G->n = n;
+    G->rows = rows;
+    for (int s = 0; s < n; s++) G->in_dims.push_back(chain[s]->in_dim);
+    const uint64_t l0 = ctx->launches;
+    cudaGraph_t graph = nullptr;
+    LKG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      run_chain(ctx, chain, n, X, rows, Y);
+    } catch (...) {
+      cudaStreamEndCapture(ctx->stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    LKG_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+    G->kernels = ctx->launches - l0;
+    ctx->launches = l0;
+    for (int s = 0; s < n; s++) ctx->rows_seen[s] = 0;  // the capture ran nothing
+    const cudaError_t e = cudaGraphInstantiate(&G->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    LKG_CUDA(e);
+    *out = G.release();
+  });
+}
+
+lkg_status lkg_graph_launch(lkg_graph* G) {
+  return guarded([&] {
+    need(G, "graph");
+    DeviceGuard g(G->ctx->device);
+    LKG_CUDA(cudaGraphLaunch(G->exec, G->ctx->stream));
+    G->ctx->launches += G->kernels;
+    for (int s = 0; s < G->n; s++) {
+      G->ctx->rows_seen[s] += (uint64_t)G->rows;
+      G->ctx->in_dim_seen[s] = G->in_dims[s];
+    }
+  });
+}
+
+lkg_status lkg_graph_destroy(lkg_graph* G) {
+  return guarded([&] {
+    if (!G) return;
+    DeviceGuard g(G->ctx->device);
+    if (G->exec) cudaGraphExecDestroy(G->exec);
+    delete G;
+  });
+}
+
 lkg_status lkg_model_forward_host(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n, const float* Xh,
                                   int64_t rows, float* Yh, lkg_oob_stats* stats) {
   return guarded([&] {

@@ -1103,7 +1103,12 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   const int64_t row_tile = (int64_t)W * 32 * R;
   a.n_rt = (rows + row_tile - 1) / row_tile;
   a.n_items = a.n_rt * gm.n_jb;
-  const int grid = (int)std::min<int64_t>(a.n_items, sm_count(ctx->device));
+  // Balanced rows (fwd_tiled BAL): one-j-block fp32 layers with codes in shared memory. Their grid
+  // spreads even a small batch over every SM (>= 64 rows per CTA): a 4096-row configs[1] batch took
+  // the time of one whole 1024-row item on each of 4 CTAs.
+  const bool bal_mode = !f64 && gm.n_jb == 1 && !gm.codes_global;
+  const int grid = bal_mode ? (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, sm_count(ctx->device)))
+                            : (int)std::min<int64_t>(a.n_items, sm_count(ctx->device));
   const size_t extra = (L2 && !gm.codes_global) ? kMaxKT * 16 + ((L2->geom.tile_bytes + 15) & ~15) : 0;
   a.ns = tiled_stages(L, W, R, extra);
   {  // row tiles per item group (item_coords). Measured on configs[3] layer 1 (1M rows): 4/8/16/32
@@ -1152,7 +1157,7 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
     ctx->launches++;
     return;
   }
-  const bool bal = !f64 && gm.n_jb == 1;  // balanced rows (fwd_tiled BAL)
+  const bool bal = bal_mode;
   switch (sel) {
 #define CASE(S)                                                                                         \
   case S:                                                                                               \

@@ -587,6 +587,37 @@ def lut_model_forward_batch(chain: list[LutLayerArtifact], X, tier: Tier = Tier.
     return ChainBatchResult(Y, st)
 
 
+class ChainGraph:
+    """A chain forward on fixed device tensors, captured once as a CUDA graph (lkg_graph_create) and
+    replayed with one cudaGraphLaunch per call — for small batches served repeatedly, where launch
+    overhead dominates. ``X`` and ``Y`` are CUDA tensors bound at capture (write new inputs into
+    ``X`` in place); OOB statistics accumulate in the engine (``engine.collect``)."""
+
+    def __init__(self, chain: list["LutLayerArtifact"], X, Y, engine: Engine | None = None):
+        if not (_is_torch(X) and X.is_cuda and _is_torch(Y) and Y.is_cuda):
+            raise DimensionError("ChainGraph binds CUDA tensors")
+        self.engine = eng = engine or default_engine(X.device.index or 0)
+        self._dev = [a.device(eng) for a in chain]
+        self.X, self.Y = X, Y
+        hs = (C.c_void_p * len(chain))(*[d.handle for d in self._dev])
+        h = C.c_void_p()
+        check(lib().lkg_graph_create(eng.handle, hs, len(chain), C.c_void_p(X.data_ptr()), X.shape[0],
+                                     C.c_void_p(Y.data_ptr()), C.byref(h)))
+        self.handle = h
+
+    def __call__(self):
+        check(lib().lkg_graph_launch(self.handle))
+        return self.Y
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                lib().lkg_graph_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
 def lut_model_forward(chain, x, tier: Tier = Tier.Optimized, engine: Engine | None = None):
     """runtime.cpp:316-325 (single row): (y, per_layer)."""
     x = np.asarray(x, np.float32).reshape(1, -1)

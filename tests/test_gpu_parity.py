@@ -640,3 +640,37 @@ def test_fuzz_spline_forward(lk, oracle, seed):
     Y = lk.layer_forward_batch(spec, X)
     Yo = oracle.spline_forward(so, X.astype(np.float64))
     assert_close(Y, Yo, f"spline fuzz {seed}: d{d} m{m} K{K} deg{deg} uniform{uniform}")
+
+
+@pytest.mark.gpu
+def test_chain_graph_replay_matches_direct(lk):
+    """lkg_graph_create / _launch (CUDA-graph replay of a chain forward) == lkg_model_forward bit for
+    bit, OOB statistics accumulate per replay, in-place input updates are seen by the replay."""
+    import torch
+    for cfg, rows in ((1, 4096), (2, 20000)):
+        dims, _, _, _ = lk.recipe_dims(cfg)
+        eng = lk.Engine(0)
+        chain = [lk.compile_layer(lk.recipe_layer(cfg, l), lk.QuantConfig(64), lk.OobConfig(), engine=eng)
+                 for l in range(len(dims) - 1)]
+        X = torch.from_numpy(lk.recipe_inputs(cfg, 0, rows)).cuda()
+        res = lk.lut_model_forward_batch(chain, X, engine=eng)
+        Y = torch.empty((rows, dims[-1]), device="cuda")
+        g = lk.ChainGraph(chain, X, Y, engine=eng)
+        eng.collect(len(chain))                      # drop what creation ran
+        for _ in range(3):
+            g()
+        eng.synchronize()
+        assert torch.equal(Y, res.Y if hasattr(res.Y, "device") else torch.from_numpy(res.Y).cuda())
+        st = eng.collect(len(chain))
+        for s_g, s_d in zip(st, res.per_layer):
+            assert s_g.n_samples == 3 * s_d.n_samples and s_g.n_oob_inputs == 3 * s_d.n_oob_inputs
+            assert s_g.n_oob_samples == 3 * s_d.n_oob_samples and s_g.n_inputs == 3 * s_d.n_inputs
+        X2 = torch.from_numpy(lk.recipe_inputs(cfg, rows, rows)).cuda()
+        X.copy_(X2)                                   # new batch in place, same graph
+        g()
+        eng.synchronize()
+        ref2 = lk.lut_model_forward_batch(chain, X2, engine=eng).Y
+        assert torch.equal(Y, ref2 if hasattr(ref2, "device") else torch.from_numpy(ref2).cuda())
+        del g
+    with pytest.raises(lk.DimensionError):
+        lk.ChainGraph(chain, X.cpu(), Y)
