@@ -674,3 +674,24 @@ def test_chain_graph_replay_matches_direct(lk):
         del g
     with pytest.raises(lk.DimensionError):
         lk.ChainGraph(chain, X.cpu(), Y)
+
+
+@pytest.mark.gpu
+def test_balanced_rows_small_batches_bit_identical(lk, oracle):
+    """One-j-block layers split any batch over every SM in 64-aligned row ranges: prefixes of a batch
+    (1 .. 5000 rows, odd sizes, fewer rows than SMs x 64) reproduce the full launch bit for bit, and
+    match the oracle within the north-star bar."""
+    for scheme in (0, 1):
+        spec = lk.recipe_layer(2, 0)
+        a = lk.compile_layer(spec, lk.QuantConfig(64, lk.Scheme(scheme), lk.Dtype(scheme)), lk.OobConfig())
+        X = lk.recipe_inputs(2, 0, 9471)
+        Yfull, sfull = lk.lut_layer_forward_batch(a, X)
+        for n in (1, 2, 63, 64, 65, 127, 1000, 5000, 9470):
+            Y, st = lk.lut_layer_forward_batch(a, X[:n])
+            assert np.array_equal(Y, Yfull[:n]), (scheme, n)
+            assert st.n_samples == n
+        so = to_oracle_spec(spec)
+        ao = oracle.compile_layer(so, 64, scheme, 1, 0, 1, 0)
+        Yo, cnt = oracle.lut_forward(ao, X[:3000].astype(np.float64))
+        assert_close(Yfull[:3000], Yo, f"balanced rows scheme {scheme}")
+        assert sfull.n_samples == 9471
