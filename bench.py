@@ -410,6 +410,22 @@ def main():
                                "algorithmic bytes = 2 code B + 4 B scale (+4 B y_min asym) per edge-eval",
                 "edge_evals_per_s": ee_k / (ms_k * 1e-3), "share_of_step": min(1.0, ms_k / ms),
                 "hbm_view": {"peak_gbs": 6547.5, "note": "LUT L2/smem-resident; DRAM traffic is X + Y (see traffic)"}}
+    # issue view: the kernel's SASS warp-instructions (ncu, scaled by rows) per second against the
+    # SM issue peak (4 schedulers x 148 SMs x clock) -- the resource that actually binds
+    wi, wi_rows = ncu_traffic(f"{key}_warp_inst"), ncu_traffic(f"{key}_warp_inst_rows")
+    if wi and wi_rows:
+        try:
+            props = torch.cuda.get_device_properties(local)
+            sms = props.multi_processor_count
+        except Exception:  # noqa: BLE001
+            sms = 148
+        inst = wi * rows / wi_rows
+        clk_mhz = 1965.0
+        roofline["issue_view"] = {"warp_inst_per_launch": inst, "achieved_warp_inst_per_s": inst / (ms_k * 1e-3),
+                                  "peak_warp_inst_per_s": 4 * sms * clk_mhz * 1e6,
+                                  "frac": inst / (ms_k * 1e-3) / (4 * sms * clk_mhz * 1e6),
+                                  "note": "ncu smsp__inst_executed of the same kernel, scaled by rows; "
+                                          "peak at the 1965 MHz max SM clock"}
 
     # same-backend honest baseline (paper §5.5): the B-spline chain forward on the same GPU and data
     spline = None
