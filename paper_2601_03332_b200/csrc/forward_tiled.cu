@@ -46,6 +46,10 @@
 #include "tma.cuh"
 #include "tmem.cuh"
 
+#ifndef LKG_NS
+#define LKG_NS 2  // fwd_tiled stage buffers (see the kernel)
+#endif
+
 namespace {
 
 using lkg::kMaxKT;
@@ -69,7 +73,6 @@ struct TiledArgs {
   unsigned long long* counters;
   lkg::CoordConst cc;        // coordinate constants (coords.cuh)
   int64_t n_items, n_rt;
-  int32_t ns;           // stage buffers (2 or 3, whatever fits shared memory)
   uint32_t rt_group;    // row tiles per item group (item_coords)
   float4 ktab[kMaxKT];  // {T_k, (L-1)/(T_k+1 - T_k), T_k+1, 0}
   // fused next layer (FUSE): a small-out_dim layer evaluated in the epilogue from the 16 hidden
@@ -116,12 +119,9 @@ template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MI
           bool BAL = false>
 __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  // Two stage buffers, a compile-time count: NS as a runtime value (a.ns) turned every per-tile
+  // Two stage buffers, a compile-time count: NS as a runtime value turned every per-tile
   // g mod NS into a 64-bit division (configs[1] layer 0: 0.567 -> 0.534 ms once removed). Three
   // (LKG_NS=3, the most that fits next to the x tiles) measured 8.5% slower on configs[1].
-#ifndef LKG_NS
-#define LKG_NS 2
-#endif
   constexpr int NS = LKG_NS;
   constexpr int ROWS_W = 32 * R;        // rows per warp
   constexpr int XS = ROWS_W + 4;        // padded row stride of the transposed x tile
@@ -1050,12 +1050,11 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
   ctx->launches++;
 }
 
-static size_t tiled_smem(const lkg_layer* L, int W, int R, int ns = 2) {
+static size_t tiled_smem(const lkg_layer* L, int W, int R, int ns = LKG_NS) {
   const int64_t sb = L->geom.tile_bytes - (L->geom.codes_global ? L->geom.p_off : 0);
   return ns * sb + (size_t)2 * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 64;
 }
 
-static int tiled_stages(const lkg_layer*, int, int, size_t) { return LKG_NS; }  // fwd_tiled's NS
 
 bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
   // Off by default: measured on C2, the fused epilogue (16 coordinates per row at the end of
@@ -1109,14 +1108,12 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   const bool bal_mode = !f64 && gm.n_jb == 1 && !gm.codes_global;
   const int grid = bal_mode ? (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, sm_count(ctx->device)))
                             : (int)std::min<int64_t>(a.n_items, sm_count(ctx->device));
-  const size_t extra = (L2 && !gm.codes_global) ? kMaxKT * 16 + ((L2->geom.tile_bytes + 15) & ~15) : 0;
-  a.ns = tiled_stages(L, W, R, extra);
   {  // row tiles per item group (item_coords). Measured on configs[3] layer 1 (1M rows): 4/8/16/32
      // within 1.5% of each other; L2 evict_last/evict_first hints on x/tiles doubled DRAM reads.
     static const char* rg = getenv("LKG_RTG");  // tuning hook
     a.rt_group = rg ? (uint32_t)std::max(1, atoi(rg)) : 8u;
   }
-  size_t smem = tiled_smem(L, W, R, a.ns);
+  size_t smem = tiled_smem(L, W, R);
   const int sel = (asym << 2) | (sr << 1) | (int)zs;
   if (gm.codes_global) {
     switch (sel) {
