@@ -492,7 +492,7 @@ def main():
                 "spline_baseline": spline,
                 "compile": {"gpu_ms": compile_ms, "layers": nl,
                             "note": "lkg_compile_layer for every layer incl. host basis tables and tile build"}}
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # the CPU baseline is an N=1 figure
             try:
                 line["cpu_baseline"] = cpu_baseline(args.workload)
             except Exception as ex:  # the oracle is optional on the box; say why it is missing
