@@ -116,7 +116,7 @@ __device__ __forceinline__ void item_coords(const TiledArgs& a, bool gc, uint32_
 }
 
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1, bool GC = false,
-          bool BAL = false>
+          bool BAL = false, int XB = 1>
 __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   // Two stage buffers, a compile-time count: NS as a runtime value turned every per-tile
@@ -133,8 +133,11 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   // from L2, and items are ordered row-tile fastest so concurrent CTAs share each tile in L2.
   const int64_t so = GC ? a.p_off : 0, sb = tb - so;
   uint8_t* stage = smem;                                                  // NS * sb
-  float* xsw = reinterpret_cast<float*>(smem + NS * sb) + warp * 2 * G * XS;  // per-warp x tiles (x2)
-  float4* ktab = reinterpret_cast<float4*>(smem + NS * sb + 2 * W * G * XS * 4);
+  // XB x-tile buffers per warp. One (the next block staged after the steps, from L1 mostly) leaves
+  // 35 KB more L1 than two (staged a tile ahead): measured C4 -7%, C3 -5%, C5 -4%, C2a -2%; only the
+  // int8 one-j-block layer (configs[1]) is faster with two (+2%).
+  float* xsw = reinterpret_cast<float*>(smem + NS * sb) + warp * XB * G * XS;
+  float4* ktab = reinterpret_cast<float4*>(smem + NS * sb + XB * W * G * XS * 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + kMaxKT);
   uint32_t* fin = reinterpret_cast<uint32_t*>(full + 4);  // warps done with each stage buffer
   float4* ktab2 = reinterpret_cast<float4*>(full + 8);
@@ -285,12 +288,14 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       // this tile's x block has landed (this lane's copies, then the warp's); prefetch the next
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncwarp();
-      const float* xs = xsw + xbuf * G * XS;
-      if (ih + 1 < a.n_ih)
-        stage_x(row0, ih + 1, xbuf ^ 1);
-      else if (li + 1 < n_local)
-        stage_x(row0_next, 0, xbuf ^ 1);
-      xbuf ^= 1;
+      const float* xs = xsw + (XB == 2 ? xbuf * G * XS : 0);
+      if constexpr (XB == 2) {
+        if (ih + 1 < a.n_ih)
+          stage_x(row0, ih + 1, xbuf ^ 1);
+        else if (li + 1 < n_local)
+          stage_x(row0_next, 0, xbuf ^ 1);
+        xbuf ^= 1;
+      }
       const int st = (int)((uint32_t)g % NS);  // constant divisor: multiply-shift
       mbar_wait(&full[st], ((uint32_t)g / NS) & 1u);
       const uint8_t* T = stage + st * sb - so;  // T + p_off is the staged P block
@@ -408,6 +413,13 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           }
           lkg::tmem_st32(tm_warp + 32 * r, w);
         }
+      }
+      if constexpr (XB == 1) {
+        __syncwarp();  // one x buffer: the next block is staged once every lane is done with this one
+        if (ih + 1 < a.n_ih)
+          stage_x(row0, ih + 1, 0);
+        else if (li + 1 < n_local)
+          stage_x(row0_next, 0, 0);
       }
       // Stage release without a CTA barrier: the last warp done with this buffer refills it, so
       // warps drift up to NS-1 stages apart instead of re-aligning at every tile.
@@ -791,12 +803,14 @@ __global__ void build_tiles_kernel(const uint8_t* q, const float* scale, const f
 }
 
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1, bool GC = false,
-          bool BAL = false>
+          bool BAL = false, int XB = 1>
 void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
-  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL>;
+  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB>;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    static const char* co = getenv("LKG_CARVEOUT");  // experiment hook: shared-memory carveout %
+    if (co) LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(co)));
     attr = true;
   }
   kern<<<grid, W * 32, smem, st>>>(a);
@@ -885,7 +899,7 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
     off += G * PROW;
   }
   off = (off + 127) / 128 * 128;
-  const size_t xs_bytes = (size_t)2 * kW * G * (32 * kR + 4) * 4;  // double-buffered x tiles
+  const size_t xs_bytes = (size_t)1 * kW * G * (32 * kR + 4) * 4;  // one x buffer (fwd_tiled XB)
   static const bool force_gc = getenv("LKG_FORCE_GC") != nullptr;  // test / tuning hook
   gm.codes_global = force_gc || 2 * off + xs_bytes + kMaxKT * 16 + 64 > 227 * 1024;  // codes stay in global (L2)
   if (gm.codes_global && 2 * (off - gm.p_off) + xs_bytes + kMaxKT * 16 + 64 > 227 * 1024) return;  // generic
@@ -1050,9 +1064,9 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
   ctx->launches++;
 }
 
-static size_t tiled_smem(const lkg_layer* L, int W, int R, int ns = LKG_NS) {
+static size_t tiled_smem(const lkg_layer* L, int W, int R, int ns = LKG_NS, int xb = 1) {
   const int64_t sb = L->geom.tile_bytes - (L->geom.codes_global ? L->geom.p_off : 0);
-  return ns * sb + (size_t)2 * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 64;
+  return ns * sb + (size_t)xb * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 64;
 }
 
 
@@ -1155,11 +1169,17 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
     return;
   }
   const bool bal = bal_mode;
+  // two x buffers only for the int8 one-j-block layers (see fwd_tiled's XB), where they fit
+  const bool xb2 = bal && !asym && tiled_smem(L, W, R, LKG_NS, 2) <= 227 * 1024;
+  if (xb2) smem = tiled_smem(L, W, R, LKG_NS, 2);
   switch (sel) {
 #define CASE(S)                                                                                         \
   case S:                                                                                               \
     if (f64)                                                                                            \
       launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true>(ctx->stream, a, smem, grid);     \
+    else if (xb2)                                                                                       \
+      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, true,              \
+                   ((S >> 2) & 1) ? 1 : 2>(ctx->stream, a, smem, grid);                                 \
     else if (bal)                                                                                       \
       launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, true>(ctx->stream, a, \
                                                                                          smem, grid);  \
