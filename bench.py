@@ -11,7 +11,7 @@ host-buffer entry point (lkg_model_forward_host: pinned X H2D, forward, Y D2H ev
 (see DESIGN.md §5). `cpu_baseline` times the reference CPU implementation (oracle/_ref =
 the reference's own sources, all host cores) on the same workload.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c2a|c3|c4] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c1|c2|c2a|c3|c4|c5] [--impl reference]
 """
 from __future__ import annotations
 
@@ -47,6 +47,7 @@ import numpy as np  # noqa: E402
 
 # workload -> (cfg, rows per GPU, L, scheme, boundary, policy)
 WORKLOADS = {
+    "c1": (1, 4_096, 64, 0, 0, 0),        # configs[0]: the tiny correctness case (latency-bound)
     "c2": (2, 1_000_000, 64, 0, 1, 0),    # configs[1], int8 symmetric
     "c2a": (2, 1_000_000, 64, 1, 1, 0),   # configs[1], uint8 asymmetric
     "c3": (3, 262_144, 64, 0, 0, 0),      # configs[2] cell L=64 sym half_open clip_x
