@@ -33,6 +33,7 @@
 //  * Coordinates: lut_coords_fast (coords.cuh) for both rows side by side, the exact path once
 //    per step for any coordinate next to a sample node; x blocks arrive by cp.async one tile
 //    ahead; items are grouped (item_coords) so x blocks and tiles are reused in L2.
+#include <cuda.h>  // CUtensorMap (the x-block tensor map of the XT mode)
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -83,6 +84,9 @@ struct TiledArgs {
   unsigned long long* counters2;
   lkg::CoordConst cc2;
   float4 ktab2[kMaxKT];
+  // XT mode: the layer input was transposed to [d][rows] (launch_forward_tiled) and each warp's x
+  // block [8 inputs][64 rows] is one 2D TMA box of this map
+  alignas(64) CUtensorMap xmap;
 };
 
 using lkg::bulk_g2s;
@@ -116,7 +120,7 @@ __device__ __forceinline__ void item_coords(const TiledArgs& a, bool gc, uint32_
 }
 
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1, bool GC = false,
-          bool BAL = false, int XB = 1>
+          bool BAL = false, int XB = 1, bool XT = false>
 __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   // Two stage buffers, a compile-time count: NS as a runtime value turned every per-tile
@@ -124,7 +128,9 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   // (LKG_NS=3, the most that fits next to the x tiles) measured 8.5% slower on configs[1].
   constexpr int NS = LKG_NS;
   constexpr int ROWS_W = 32 * R;        // rows per warp
-  constexpr int XS = ROWS_W + 4;        // padded row stride of the transposed x tile
+  // row stride of the transposed x tile: padded for the 4-byte cp.async writes, or exactly the TMA
+  // box (XT; the rotated reads xs[il][lane + 32r] are conflict-free either way)
+  constexpr int XS = XT ? ROWS_W : ROWS_W + 4;
   constexpr int NXL = ROWS_W / 4;        // x elements each lane stages per tile (cp.async)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t tb = a.tile_bytes;
@@ -140,7 +146,8 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   float4* ktab = reinterpret_cast<float4*>(smem + NS * sb + XB * W * G * XS * 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + kMaxKT);
   uint32_t* fin = reinterpret_cast<uint32_t*>(full + 4);  // warps done with each stage buffer
-  float4* ktab2 = reinterpret_cast<float4*>(full + 8);
+  uint64_t* xbar = full + 8;  // XT: per-warp x-block barriers (W <= 16)
+  float4* ktab2 = reinterpret_cast<float4*>(full + 24);
   uint8_t* lut2 = reinterpret_cast<uint8_t*>(ktab2 + kMaxKT);
 
   for (int k = tid; k < a.cc.K; k += W * 32) ktab[k] = a.ktab[k];
@@ -154,6 +161,8 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       mbar_init(&full[s], 1);
       fin[s] = 0;
     }
+    if (XT)
+      for (int w = 0; w < W; w++) mbar_init(&xbar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // F64: the f64 accumulators live in Tensor Memory (tmem.cuh), not registers: each thread owns
@@ -225,7 +234,20 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
     item_coords(a, GC, item_, rt_, jb_);
     return (int64_t)rt_ * (W * ROWS_W) + warp * ROWS_W;
   };
+  uint32_t xphase = 0;
   auto stage_x = [&](int64_t r0_, int ih_, int buf) {
+    if constexpr (XT) {  // one 2D TMA box [8 inputs][64 rows] of the transposed input
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the warp's reads, then TMA writes
+        mbar_expect_tx(&xbar[warp], (uint32_t)(G * ROWS_W * 4));
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+            ::"r"(lkg::smem_u32(xsw + buf * G * XS)), "l"(&a.xmap), "r"((int)r0_), "r"(ih_ * G),
+            "r"(lkg::smem_u32(&xbar[warp]))
+            : "memory");
+      }
+      return;
+    }
     const int c_ = lane & 7, i_ = ih_ * G + c_;
     float* dst = xsw + buf * G * XS + c_ * XS + (lane >> 3);
     int64_t col_ = i_;
@@ -286,7 +308,12 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
 
     for (int ih = 0; ih < a.n_ih; ih++, g++) {
       // this tile's x block has landed (this lane's copies, then the warp's); prefetch the next
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      if constexpr (XT) {
+        mbar_wait(&xbar[warp], xphase);
+        xphase ^= 1u;
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
       __syncwarp();
       const float* xs = xsw + (XB == 2 ? xbuf * G * XS : 0);
       if constexpr (XB == 2) {
@@ -803,9 +830,9 @@ __global__ void build_tiles_kernel(const uint8_t* q, const float* scale, const f
 }
 
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1, bool GC = false,
-          bool BAL = false, int XB = 1>
+          bool BAL = false, int XB = 1, bool XT = false>
 void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
-  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB>;
+  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT>;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -1066,7 +1093,7 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
 
 static size_t tiled_smem(const lkg_layer* L, int W, int R, int ns = LKG_NS, int xb = 1) {
   const int64_t sb = L->geom.tile_bytes - (L->geom.codes_global ? L->geom.p_off : 0);
-  return ns * sb + (size_t)xb * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 64;
+  return ns * sb + (size_t)xb * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 64 + 8 * 16;
 }
 
 
@@ -1083,6 +1110,44 @@ bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
   if (L1->in_dim > kFp32MaxD || L2->in_dim != L1->col1 - L1->col0 || L2->col1 - L2->col0 > 8) return false;
   if (L1->scheme != L2->scheme || L1->value_repr != L2->value_repr || L1->oob_policy != L2->oob_policy) return false;
   return tiled_smem(L1, kW, kR) + kMaxKT * 16 + ((g2.tile_bytes + 15) & ~15) <= 227 * 1024;
+}
+
+// X [rows][d] -> Xt [d][rows] (32x32 tiles through shared memory, both sides coalesced).
+__global__ void transpose_kernel(const float* __restrict__ X, int64_t rows, int32_t d, float* __restrict__ Xt) {
+  __shared__ float t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + k;
+    const int c = c0 + threadIdx.x;
+    if (r < rows && c < d) t[k][threadIdx.x] = X[r * d + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = c0 + k;
+    const int64_t r = r0 + threadIdx.x;
+    if (r < rows && c < d) Xt[(int64_t)c * rows + r] = t[threadIdx.x][k];
+  }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
+static void encode_x_map(CUtensorMap* map, const float* Xt, int64_t rows, int d, int box_rows, int box_cols) {
+  typedef CUresult (*Encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    LKG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q));
+    if (!enc || q != cudaDriverEntryPointSuccess) throw Error{LKG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable"};
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)d};
+  const cuuint64_t strides[1] = {(cuuint64_t)rows * sizeof(float)};
+  const cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols}, es[2] = {1u, 1u};
+  if (enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(Xt), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    throw Error{LKG_ERR_CUDA, "cuTensorMapEncodeTiled failed"};
 }
 
 void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk, float* Y,
@@ -1129,6 +1194,41 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   }
   size_t smem = tiled_smem(L, W, R);
   const int sel = (asym << 2) | (sr << 1) | (int)zs;
+  // XT: layers that re-read every x block for many j-blocks take their input transposed once
+  // ([d][rows], one extra pass over X) so each warp's x block is a single 2D TMA box in whole
+  // bursts: no per-lane copies, no L1 allocation, half the DRAM traffic. Whole row tiles
+  // and input tiles only (no padding rows or inputs to keep out of the OOB counts). Measured: C4
+  // layer (64 j-blocks) 457.5 -> 445.9 ms incl. the transpose; C3 layer 0 (4 j-blocks) +3% (the
+  // transpose outweighs the gain), hence the j-block threshold.
+  static const char* xt_env = getenv("LKG_XT");  // LKG_XT=0 disables (A/B hook)
+  const bool xt = !(xt_env && xt_env[0] == '0') && !gm.codes_global && !L2 && gm.n_jb >= 16 && x_blk <= 0 &&
+                  rows % row_tile == 0 && L->in_dim % G == 0 && rows < (1ll << 31);
+  if (xt) {
+    if (ctx->xt.bytes < sizeof(float) * (size_t)rows * L->in_dim) ctx->xt.alloc(sizeof(float) * (size_t)rows * L->in_dim);
+    float* Xt = ctx->xt.as<float>();
+    transpose_kernel<<<dim3((unsigned)((rows + 31) / 32), (unsigned)((L->in_dim + 31) / 32)), dim3(32, 8), 0,
+                       ctx->stream>>>(X, rows, L->in_dim, Xt);
+    LKG_CUDA(cudaGetLastError());
+    ctx->launches++;
+    encode_x_map(&a.xmap, Xt, rows, L->in_dim, 32 * R, G);
+    a.X = Xt;
+    switch (sel) {
+#define CASE(S)                                                                                                \
+  case S:                                                                                                      \
+    if (f64)                                                                                                   \
+      launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, false, false, 1, true>(      \
+          ctx->stream, a, smem, grid);                                                                         \
+    else                                                                                                       \
+      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, false, 1, true>(         \
+          ctx->stream, a, smem, grid);                                                                         \
+    break;
+      CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+    }
+    LKG_CUDA(cudaGetLastError());
+    ctx->launches++;
+    return;
+  }
   if (gm.codes_global) {
     switch (sel) {
 #define CASE(S)                                                                                                \

@@ -695,3 +695,24 @@ def test_balanced_rows_small_batches_bit_identical(lk, oracle):
         Yo, cnt = oracle.lut_forward(ao, X[:3000].astype(np.float64))
         assert_close(Yfull[:3000], Yo, f"balanced rows scheme {scheme}")
         assert sfull.n_samples == 9471
+
+
+@pytest.mark.gpu
+def test_transposed_input_walk_bit_identical(lk, oracle):
+    """Layers with many j-blocks (>= 16) take their input transposed through 2D TMA boxes when the
+    batch is whole 1024-row tiles (XT mode): same bits as the row-major path (a batch one row short
+    takes that path), OOB counts equal, and the oracle's outputs within the north-star bar."""
+    import torch
+    spec = lk.recipe_layer(4, 1)                  # 1024 -> 1024, 64 j-blocks, f64 accumulators
+    a = lk.compile_layer(spec, lk.QuantConfig(64), lk.OobConfig(lk.BoundaryMode.HalfOpen, lk.OobPolicy.ClipX))
+    g = torch.Generator().manual_seed(7)
+    X = (torch.rand((2048, 1024), generator=g) * 2.6 - 1.3).numpy().astype(np.float32)
+    Yt, st = lk.lut_layer_forward_batch(a, torch.from_numpy(X).cuda())       # XT
+    Yr, sr = lk.lut_layer_forward_batch(a, torch.from_numpy(X[:2047]).cuda())  # row-major path
+    Yt, Yr = Yt.cpu().numpy(), Yr.cpu().numpy()
+    assert np.array_equal(Yt[:2047], Yr)
+    assert st.n_samples == 2048 and sr.n_samples == 2047
+    assert st.n_oob_inputs >= sr.n_oob_inputs and st.n_oob_inputs - sr.n_oob_inputs <= 1024
+    ao = oracle.compile_layer(to_oracle_spec(spec), 64, 0, 1, 0, 0, 0)
+    Yo, cnt = oracle.lut_forward(ao, X[2000:2048].astype(np.float64))
+    assert_close(Yt[2000:2048], Yo, "XT walk vs oracle")
