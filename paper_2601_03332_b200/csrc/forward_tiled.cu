@@ -1201,8 +1201,11 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   // layer (64 j-blocks) 457.5 -> 445.9 ms incl. the transpose; C3 layer 0 (4 j-blocks) +3% (the
   // transpose outweighs the gain), hence the j-block threshold.
   static const char* xt_env = getenv("LKG_XT");  // LKG_XT=0 disables (A/B hook)
-  const bool xt = !(xt_env && xt_env[0] == '0') && !gm.codes_global && !L2 && gm.n_jb >= 16 && x_blk <= 0 &&
-                  rows % row_tile == 0 && L->in_dim % G == 0 && rows < (1ll << 31);
+  // codes-in-L2 (GC) layers take XT too when they have f64 accumulators (C5 layer 0: -4.4 % time;
+  // the row-major x staging shares L1 with the __ldg code reads there)
+  const bool xt_gc_ok = f64;
+  const bool xt = !(xt_env && xt_env[0] == '0') && (!gm.codes_global || xt_gc_ok) && !L2 && gm.n_jb >= 16 &&
+                  x_blk <= 0 && rows % row_tile == 0 && L->in_dim % G == 0 && rows < (1ll << 31);
   if (xt) {
     if (ctx->xt.bytes < sizeof(float) * (size_t)rows * L->in_dim) ctx->xt.alloc(sizeof(float) * (size_t)rows * L->in_dim);
     float* Xt = ctx->xt.as<float>();
@@ -1215,7 +1218,10 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
     switch (sel) {
 #define CASE(S)                                                                                                \
   case S:                                                                                                      \
-    if (f64)                                                                                                   \
+    if (f64 && gm.codes_global)                                                                                \
+      launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, true, false, 1, true>(       \
+          ctx->stream, a, smem, grid);                                                                         \
+    else if (f64)                                                                                              \
       launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, false, false, 1, true>(      \
           ctx->stream, a, smem, grid);                                                                         \
     else                                                                                                       \

@@ -716,3 +716,24 @@ def test_transposed_input_walk_bit_identical(lk, oracle):
     ao = oracle.compile_layer(to_oracle_spec(spec), 64, 0, 1, 0, 0, 0)
     Yo, cnt = oracle.lut_forward(ao, X[2000:2048].astype(np.float64))
     assert_close(Yt[2000:2048], Yo, "XT walk vs oracle")
+
+
+def test_transposed_input_walk_codes_in_l2_bit_identical(lk, oracle):
+    """C5 geometry (L=128 uint8 asym, codes read from L2: the GC kernel) on 1024 output columns
+    (>= 16 j-blocks): whole 1024-row tiles take the transposed-input (XT) walk, a batch one row short
+    the row-major one; the same bits, and the oracle on a column slice within the north-star bar."""
+    import torch
+    spec = lk.recipe_layer(5, 0, 0, 1024)
+    g = lk.compile_layer(spec, lk.QuantConfig(128, lk.Scheme.Asymmetric, lk.Dtype.Uint8),
+                         lk.OobConfig(lk.BoundaryMode.Closed, lk.OobPolicy.ZeroSpline))
+    X = lk.recipe_inputs(5, 0, 2048)
+    Yt, st = lk.lut_layer_forward_batch(g, torch.from_numpy(X).cuda())
+    Yr, sr = lk.lut_layer_forward_batch(g, torch.from_numpy(X[:2047]).cuda())
+    del g
+    Yt, Yr = Yt.cpu().numpy(), Yr.cpu().numpy()
+    assert np.array_equal(Yt[:2047], Yr)
+    assert st.n_samples == 2048 and sr.n_samples == 2047
+    c0, c1 = 1016, 1024
+    ao = oracle.compile_layer(to_oracle_spec(lk.recipe_layer(5, 0, c0, c1)), 128, 1, 1, 0, 1, 1)
+    Yo, _ = oracle.lut_forward(ao, X[2016:2048].astype(np.float64), nthreads=8)
+    assert_close(Yt[2016:2048, c0:c1], Yo, "GC XT walk vs oracle")
