@@ -54,6 +54,9 @@ WORKLOADS = {
     "c4": (4, 1_048_576, 64, 0, 0, 0),    # configs[3]: the full batch, sharded over the ranks
     "c5": (5, 16_384, 128, 1, 1, 1),      # configs[4]: column-sharded over the ranks, NCCL all-gather
 }
+# BASELINE.json configs[cfg-1]: (widths, G)
+RECIPE_SHAPES = {1: ([2, 5, 1], 5), 2: ([78, 16, 2], 5), 3: ([64, 64, 1], 8), 4: ([1024, 1024, 1024, 10], 8),
+                 5: ([4096, 4096, 4096], 16)}
 # workloads whose BASELINE batch is fixed and split over the GPUs (strong scaling); the others give
 # every rank its own full batch (weak scaling)
 STRONG = {"c4"}
@@ -116,6 +119,21 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def workload_config(wl, world):
+    """The `config` dict of a workload, identical in both arms (the driver compares them)."""
+    cfg, rows, L, scheme, bm, op = WORKLOADS[wl]
+    dims, G = RECIPE_SHAPES[cfg]
+    strong = wl in STRONG or wl == "c5"
+    total = rows if strong else rows * world
+    return {"workload": wl, "cfg": f"configs[{cfg - 1}]", "dims": dims, "G": G, "L": L,
+            "scheme": ["int8_symmetric", "uint8_asymmetric"][scheme],
+            "boundary_mode": ["half_open", "closed"][bm], "oob_policy": ["clip_x", "zero_spline"][op],
+            "rows": total, "rows_per_gpu": total // world if strong else rows,
+            "parallelism": (f"output-column shards x{world}, NCCL all-gather" if wl == "c5"
+                            else f"batch dp{world}, LUT replicated"),
+            "l2": "inputs larger than L2 (no flush)"}
+
+
 def run_reference(args, wl):
     """--impl reference: the reference CPU implementation of the path on the host cores."""
     rank = _env_int("RANK", 0)
@@ -144,11 +162,11 @@ def run_reference(args, wl):
             "unit": "edge-evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (BASELINE recipe, reference Rng)",
-            "config": {"workload": wl, "cfg": f"configs[{cfg - 1}]", "dims": dims, "L": L,
-                       "scheme": ["int8_symmetric", "uint8_asymmetric"][scheme], "rows_per_step": sample_rows},
+            "config": workload_config(wl, _env_int("WORLD_SIZE", 1)),
             "cpu_baseline": {"value": value, "unit": "edge-evals/s", "cores": nthreads, "kind": o.kind,
                              "sample": f"{sample_rows} rows of {wl} per step (reference lut_model_forward_batch, "
-                                       f"Tier::Optimized, rows sharded over {nthreads} threads)"},
+                                       f"Tier::Optimized, rows sharded over {nthreads} threads); the "
+                                       f"rate is flat in the row count (row-outer loop)"},
             "e2e": {"value": value, "unit": "edge-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
@@ -204,6 +222,32 @@ def cpu_baseline(wl):
             "single_thread": {"value": n1 * ee_row / sec1, "unit": "edge-evals/s", "cores": 1,
                               "sample": f"{n1} rows, one thread (the reference's timing protocol)"},
             "compile_s": compile_s, "compile_note": f"reference compile_layer of the {nl}-layer chain, one thread"}
+
+
+def argmax_report(wl, X, hidden, Y, Y_spline):
+    """configs[1]'s required report (BASELINE.json): argmax agreement of the GPU LUT chain on the
+    full batch against the reference's CPU LUT chain (SURVEY §8c protocol: every mismatch explained
+    by a logit near-tie or a knot straddle of a hidden value, oracle/agreement.py) and against the
+    B-spline model it was compiled from (the same-GPU spline chain). Checker only: runs after the
+    timed regions, on rank 0 at N=1."""
+    from oracle.agreement import chain_agreement
+    from oracle.pyoracle import Oracle
+    cfg, rows, L, scheme, bm, op = WORKLOADS[wl]
+    o = Oracle("auto")
+    nl = len(o_dims(cfg)) - 1
+    chain = [o.compile_layer(o.recipe_layer(cfg, l), L, scheme, 1, 0, bm, op) for l in range(nl)]
+    t0 = time.perf_counter()
+    rep = chain_agreement(o, chain, X, hidden, Y, os.cpu_count() or 1)
+    out = {"rows": rep["rows"],
+           "vs_cpu_lut": {"agree": rep["agree"], "mismatch": rep["mismatch"], "near_tie": rep["near_tie"],
+                          "knot_straddle": rep["knot_straddle"], "unexplained": rep["unexplained"],
+                          "frac": rep["agreement"], "checker": o.kind},
+           "check_s": time.perf_counter() - t0}
+    if Y_spline is not None:
+        out["vs_spline"] = {"agree": int(np.sum(np.argmax(Y_spline, 1) == np.argmax(Y, 1))),
+                            "frac": float(np.mean(np.argmax(Y_spline, 1) == np.argmax(Y, 1))),
+                            "spline": "same-GPU B-spline chain (K3) on the same rows"}
+    return out
 
 
 def run_c5(args):
@@ -269,10 +313,9 @@ def run_c5(args):
         line = {"metric": METRIC, "value": ee / (ms * 1e-3),
                 "unit": "edge-evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "u8 codes, fp32 math, f64 accumulation", "data": "synthetic (BASELINE.json recipe)",
-                "config": {"workload": "c5", "cfg": "configs[4]", "dims": dims, "G": G, "L": L,
-                           "scheme": "uint8_asymmetric", "boundary_mode": "closed", "oob_policy": "zero_spline",
-                           "rows": rows, "parallelism": f"output-column shards x{world}, NCCL all-gather"},
+                "dtype": "u8 codes; fp32 per-term math; fp32 partials over 8 inputs flushed to f64 (TMEM)",
+                "data": "synthetic (BASELINE.json recipe)",
+                "config": workload_config("c5", world),
                 "roofline": {"bound": "smem", "achieved": achieved, "peak": SMEM_PEAK_GBS, "unit": "GB/s",
                              "frac": achieved / SMEM_PEAK_GBS, "traffic": ncu_traffic("c5/layer0"),
                              "kernel": "per-rank step (2 column-shard layer forwards + all-gather)"},
@@ -283,6 +326,19 @@ def run_c5(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def relaunch_distributed(argv, n):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: run the same command as N ranks, one
+    process per GPU (torch.distributed.run on 127.0.0.1, a free port), and pass rank 0's JSON line
+    through. Under torchrun (WORLD_SIZE set) the ranks run main() directly."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -429,8 +485,20 @@ def main():
                                   "note": "ncu smsp__inst_executed of the same kernel, scaled by rows; "
                                           "peak at the 1965 MHz max SM clock"}
 
+    # hidden activations of the last full forward, for the argmax report's per-layer diagnostics
+    hidden, cur = [], Xd
+    for l in range(nl - 1):
+        Hl = torch.empty((rows, dims[l + 1]), dtype=torch.float32, device=f"cuda:{local}")
+        lk.lutkan.check(lib().lkg_layer_forward(eng.handle, dev[l].handle, C.c_void_p(cur.data_ptr()), rows,
+                                                C.c_void_p(Hl.data_ptr()), None))
+        hidden.append(Hl)
+        cur = Hl
+    torch.cuda.synchronize()
+    hidden = [h.cpu().numpy() for h in hidden]
+    eng.collect(nl)
+
     # same-backend honest baseline (paper §5.5): the B-spline chain forward on the same GPU and data
-    spline = None
+    spline, spline_out = None, None
     if not args.no_spline:
         sdev = [sp.device(eng) for sp in specs]
         bufs = [Xd] + [torch.empty((rows, dims[l + 1]), dtype=torch.float32, device=f"cuda:{local}")
@@ -449,6 +517,7 @@ def main():
         e1.record(stream)
         barrier()
         ms_s = e0.elapsed_time(e1) / ks
+        spline_out = bufs[nl].cpu().numpy()
         spline = {"value": rows * ee_row / (ms_s * 1e-3), "unit": "edge-evals/s", "ms_per_step": ms_s,
                   "lut_speedup": ms_s / ms, "kernel": "spline_forward (Cox-de Boor, fp32 terms, f64 accumulation)"}
 
@@ -481,14 +550,13 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "edge-evals/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong" if args.workload in STRONG else "weak",
-                "vs_baseline": None, "dtype": "u8/i8 codes, fp32 math",
+                "vs_baseline": None,
+                "dtype": ("u8/i8 codes; fp32 per-term math; " +
+                          ("fp32 accumulation (d <= 256)" if max(dims[:-1]) <= 256 else
+                           "fp32 accumulation for d <= 256, fp32 partials over 8 inputs flushed to f64 "
+                           "accumulators in TMEM for d > 256")),
                 "data": "synthetic (BASELINE.json recipe, reference Rng; inputs > L2, no flush)",
-                "config": {"workload": args.workload, "cfg": f"configs[{cfg - 1}]", "dims": dims, "G": G, "L": L,
-                           "scheme": ["int8_symmetric", "uint8_asymmetric"][scheme],
-                           "boundary_mode": ["half_open", "closed"][bm], "oob_policy": ["clip_x", "zero_spline"][op],
-                           "rows": total_rows, "rows_per_gpu": rows,
-                           "parallelism": f"batch dp{world}, LUT replicated",
-                           "l2": "inputs larger than L2 (no flush)"},
+                "config": workload_config(args.workload, world),
                 "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
                 "oob_any_frac_layer0": stats[0].oob_any_frac(), "clocks": clk.summary(),
                 "spline_baseline": spline,
@@ -499,6 +567,12 @@ def main():
                 line["cpu_baseline"] = cpu_baseline(args.workload)
             except Exception as ex:  # the oracle is optional on the box; say why it is missing
                 line["cpu_baseline"] = {"value": None, "error": repr(ex)}
+            if args.workload in ("c2", "c2a", "c1"):
+                try:
+                    line["argmax_agreement"] = argmax_report(args.workload, Xh.numpy(), hidden, Yd.cpu().numpy(),
+                                                             spline_out)
+                except Exception as ex:  # noqa: BLE001
+                    line["argmax_agreement"] = {"error": repr(ex)}
         emit(line)
     if dist:
         dist.barrier()
@@ -506,5 +580,13 @@ def main():
 
 
 if __name__ == "__main__":
+    _n = 1
+    for _i, _a in enumerate(sys.argv):
+        if _a == "--gpus" and _i + 1 < len(sys.argv):
+            _n = int(sys.argv[_i + 1])
+        elif _a.startswith("--gpus="):
+            _n = int(_a.split("=", 1)[1])
+    if _n > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(sys.argv[1:], _n))
     isolate_stdout()
     main()

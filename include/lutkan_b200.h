@@ -18,9 +18,13 @@
  *  - Layouts are the reference's: edges input-major e = i*out_dim + j (spline.hpp:43),
  *    q_table [E,K,L], scale/y_min [E,K], knots [K+1] (runtime.hpp:31-63).
  *  - Device-resident objects (lkg_layer, lkg_spec) are immutable after creation and
- *    may be shared by contexts on the same device. A context owns one CUDA stream;
- *    all work is stream-ordered on it. Distinct contexts may be driven from distinct
- *    host threads (the reference is pure and re-entrant).
+ *    may be shared by contexts on the same device and by any number of host threads.
+ *  - Threading contract: ONE lkg_ctx PER HOST THREAD. A context owns one CUDA stream, its
+ *    scratch buffers and its OOB counters; all work is stream-ordered on it and a context
+ *    must not be driven by two threads at once. Distinct contexts may be driven from
+ *    distinct host threads concurrently, which is how the reference's purity and
+ *    re-entrancy is kept: the C++ shim (lutkan_b200.hpp) gives every
+ *    host thread its own default context.
  *  - Documented differences from the reference: activations are fp32 on the device
  *    (the reference's Matrix is f64; parity inputs are fp32-representable, so segment
  *    indices and OOB masks are bit-exact); Tier is accepted by the C++ shim and
@@ -184,8 +188,10 @@ lkg_status lkg_model_forward_host(lkg_ctx* ctx, const lkg_layer* const* chain, i
  * lkg_model_forward on the same DEVICE buffers (X, Y and the layers are bound at capture; rows > 0),
  * one cudaGraphLaunch per replay on ctx's stream, asynchronous. For small, latency-bound batches
  * served repeatedly. Creation runs the chain once eagerly (sizes scratch, sets kernel attributes).
- * OOB statistics of the replays accumulate in ctx like direct calls (lkg_ctx_collect). The layers,
- * X and Y must outlive the graph. */
+ * The graph owns its hidden-activation and transposed-input buffers, so other forwards on ctx
+ * (any batch size or width) never invalidate it. OOB statistics of the replays accumulate in ctx
+ * like direct calls (lkg_ctx_collect). The layers, X and Y must outlive the graph; replays of one
+ * graph are stream-ordered on ctx's stream. */
 typedef struct lkg_graph lkg_graph;
 lkg_status lkg_graph_create(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n_layers, const float* X,
                             int64_t rows, float* Y, lkg_graph** out);

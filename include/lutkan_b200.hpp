@@ -14,7 +14,8 @@
 //
 // Documented differences: activations cross to the device as fp32 (results are widened back to
 // f64 in the returned Matrix); Tier is accepted and ignored (one backend, no CPU fallback).
-// Device copies of artifacts are cached per Artifact address for the lifetime of the Context.
+// Device copies of artifacts are cached per Artifact address for the lifetime of the Context;
+// every host thread has its own default Context, so concurrent calls are safe as in the reference.
 #pragma once
 
 #include <cstdint>
@@ -55,7 +56,8 @@ inline void check(lkg_status st) {
   }
 }
 
-// One CUDA context (device + stream) and its device-resident artifacts.
+// One CUDA context (device + stream) and its device-resident artifacts. Not thread-safe: one
+// Context per host thread (default_context() is thread_local).
 class Context {
  public:
   explicit Context(int device = 0) { check(lkg_ctx_create(device, nullptr, &ctx_)); }
@@ -187,8 +189,14 @@ class Context {
   std::map<const void*, uint64_t> layer_fp_, spec_fp_;
 };
 
+// The default context is PER HOST THREAD: a Context (one lkg_ctx: stream, scratch buffers, OOB
+// counters, artifact cache) must never be driven by two threads at once (lutkan_b200.h threading
+// contract), so each thread calling the reference-signature functions below gets its own. That
+// keeps the reference's guarantee that these functions are pure and safe to call concurrently
+// (test_spline.cpp:310-323). A thread's context and its device copies of the
+// artifacts it used are released when the thread exits.
 inline Context& default_context() {
-  static Context ctx(0);
+  static thread_local Context ctx(0);
   return ctx;
 }
 

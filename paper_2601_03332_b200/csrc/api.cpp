@@ -643,6 +643,23 @@ struct lkg_graph {
   int64_t rows = 0;
   uint64_t kernels = 0;          // launches per replay
   std::vector<int32_t> in_dims;  // per layer slot (OobStats bookkeeping of each replay)
+  // The graph's own hidden-activation and transposed-input buffers: the replayed kernels (and the
+  // XT tensor map baked into their parameters) keep pointing at these, so later forwards on the
+  // same context may grow or free the context's buffers freely.
+  lkg::DBuf scratch[2], xt;
+};
+
+// Swaps the graph's buffers into the context for the eager pass and the capture, and back out.
+struct GraphBuffers {
+  lkg_ctx* ctx;
+  lkg_graph* G;
+  GraphBuffers(lkg_ctx* c, lkg_graph* g) : ctx(c), G(g) { swap(); }
+  ~GraphBuffers() { swap(); }
+  void swap() {
+    ctx->scratch[0].swap(G->scratch[0]);
+    ctx->scratch[1].swap(G->scratch[1]);
+    ctx->xt.swap(G->xt);
+  }
 };
 
 lkg_status lkg_graph_create(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n, const float* X, int64_t rows,
@@ -656,13 +673,14 @@ lkg_status lkg_graph_create(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t
     need(X, "X");
     need(Y, "Y");
     DeviceGuard g(ctx->device);
-    // one eager pass first: scratch buffers sized, kernel attributes set (neither is a stream
+    auto G = std::make_unique<lkg_graph>();
+    GraphBuffers own(ctx, G.get());
+    // one eager pass first: the graph's buffers sized, kernel attributes set (neither is a stream
     // operation a capture could record), and the chain validated
     run_chain(ctx, chain, n, X, rows, Y);
     LKG_CUDA(cudaStreamSynchronize(ctx->stream));
     reset_slots(ctx, n);
     for (int s = 0; s < n; s++) ctx->rows_seen[s] = 0;
-    auto G = std::make_unique<lkg_graph>();
     G->ctx = ctx;
     G->n = n;
     G->rows = rows;
@@ -705,6 +723,7 @@ lkg_status lkg_graph_destroy(lkg_graph* G) {
   return guarded([&] {
     if (!G) return;
     DeviceGuard g(G->ctx->device);
+    cudaStreamSynchronize(G->ctx->stream);  // no replay still reads the graph's buffers
     if (G->exec) cudaGraphExecDestroy(G->exec);
     delete G;
   });
@@ -1159,6 +1178,11 @@ lkg_status lkg_model_forward_sharded(lkg_ctx* ctx, const lkg_layer* const* chain
     // communication stream while layer l computes chunk c+1, and layer l+1 starts on chunk c as
     // soon as its gather lands. Per chunk the gathered activations are rank-major blocks
     // [G][rows_c][m_l] (ncclAllGather's layout), consumed in place by the next layer.
+    // Chunk c owns a FIXED region of scratch (rows from r0 at the widest local width) and of the
+    // gather buffer (at the widest full width) in every layer: layer l+1's chunk c then only
+    // touches memory whose last users (layer l's chunk-c kernel and gather) it already waits on,
+    // whatever the widths (a region packed by each layer's own width let a widening layer
+    // overwrite chunks c+1.. of the previous layer while their gathers were in flight).
     static const char* chunk_env = getenv("LKG_SHARD_CHUNKS");
     int nch = chunk_env ? atoi(chunk_env) : (G > 1 && rows >= 8192 ? 4 : 1);
     nch = (int)std::max<int64_t>(1, std::min<int64_t>(nch, std::max<int64_t>(rows, 1)));
@@ -1180,9 +1204,9 @@ lkg_status lkg_model_forward_sharded(lkg_ctx* ctx, const lkg_layer* const* chain
       for (int c = 0; c < nch; c++) {
         const int64_t r0 = c * rc, rn = std::min(rc, rows - r0);
         if (rn <= 0) break;
-        const float* in = l == 0 ? X + r0 * chain[0]->in_dim : ctx->gather.as<float>() + (int64_t)G * r0 * m_prev;
+        const float* in = l == 0 ? X + r0 * chain[0]->in_dim : ctx->gather.as<float>() + (int64_t)G * r0 * (int64_t)full;
         if (l > 0 && nch > 1) LKG_CUDA(cudaStreamWaitEvent(ctx->stream, prev_gathered[c], 0));
-        float* dst = last ? Y + r0 * m_l : ctx->scratch[0].as<float>() + r0 * m_l;
+        float* dst = last ? Y + r0 * m_l : ctx->scratch[0].as<float>() + r0 * (int64_t)loc;
         lkg::launch_forward(ctx, chain[l], in, rn, l == 0 ? 0 : (int32_t)m_prev, dst, l, true);
         if (last) continue;
         if (nch > 1) {
@@ -1190,7 +1214,7 @@ lkg_status lkg_model_forward_sharded(lkg_ctx* ctx, const lkg_layer* const* chain
           LKG_CUDA(cudaEventRecord(done, ctx->stream));
           LKG_CUDA(cudaStreamWaitEvent(cs, done, 0));
         }
-        float* gdst = ctx->gather.as<float>() + (int64_t)G * r0 * m_l;
+        float* gdst = ctx->gather.as<float>() + (int64_t)G * r0 * (int64_t)full;
         const size_t cnt = (size_t)rn * m_l;
         if (ctx->nccl) {
           const ncclResult_t r = ncclAllGather(dst, gdst, cnt, ncclFloat, static_cast<ncclComm_t>(ctx->nccl), cs);

@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/lutkan_b200.h"
@@ -53,6 +54,10 @@ struct DBuf {
   }
   template <class T>
   T* as() const { return static_cast<T*>(p); }
+  void swap(DBuf& o) {
+    std::swap(p, o.p);
+    std::swap(bytes, o.bytes);
+  }
 };
 
 // Forward-kernel tile geometry chosen at upload time (forward.cu).

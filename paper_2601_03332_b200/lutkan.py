@@ -535,6 +535,27 @@ class ChainBatchResult:
     per_layer: list
 
 
+def _torch_enter(eng: Engine, t):
+    """Order the engine's stream after torch's current stream on t's device (an X produced by an
+    asynchronous torch kernel, or the copy .contiguous().float() just made, is complete before the
+    library reads it); returns the engine stream as a torch stream."""
+    import torch
+    dev = t.device
+    ext = torch.cuda.ExternalStream(eng.stream, device=dev) if eng.stream else torch.cuda.default_stream(dev)
+    ext.wait_stream(torch.cuda.current_stream(dev))
+    return ext
+
+
+def _torch_exit(ext, *tensors):
+    """Order torch's current stream after the engine's work, and keep the tensors the engine read
+    or wrote alive for the caching allocator until that work is done."""
+    import torch
+    dev = tensors[0].device
+    torch.cuda.current_stream(dev).wait_stream(ext)
+    for t in tensors:
+        t.record_stream(ext)
+
+
 def _forward(chain, X, engine: Engine | None):
     eng = engine or default_engine()
     if not chain:
@@ -552,8 +573,10 @@ def _forward(chain, X, engine: Engine | None):
             raise DimensionError("batch column count does not match artifact in_dim")
         X = X.contiguous().float()
         Y = torch.empty((X.shape[0], m_out), device=X.device, dtype=torch.float32)
+        ext = _torch_enter(eng, X)
         check(lib().lkg_model_forward(eng.handle, handles, len(layers), C.c_void_p(X.data_ptr()), X.shape[0],
                                       C.c_void_p(Y.data_ptr()), stats))
+        _torch_exit(ext, X, Y)
     else:
         X = np.asarray(X)
         if X.ndim != 2 or X.shape[1] != chain[0].in_dim:
@@ -606,7 +629,9 @@ class ChainGraph:
         self.handle = h
 
     def __call__(self):
+        ext = _torch_enter(self.engine, self.X)  # X may have been rewritten in place by torch
         check(lib().lkg_graph_launch(self.handle))
+        _torch_exit(ext, self.Y)
         return self.Y
 
     def __del__(self):
@@ -637,8 +662,10 @@ def layer_forward_batch(layer: KanLayerSpec, X, tier: Tier = Tier.Optimized, eng
             raise DimensionError("batch column count does not match in_dim")
         X = X.contiguous().float()
         Y = torch.empty((X.shape[0], layer.out_dim), device=X.device, dtype=torch.float32)
+        ext = _torch_enter(eng, X)
         check(lib().lkg_spline_forward(eng.handle, spec.handle, C.c_void_p(X.data_ptr()), X.shape[0],
                                        C.c_void_p(Y.data_ptr())))
+        _torch_exit(ext, X, Y)
         return Y
     X = np.asarray(X)
     if X.ndim != 2 or X.shape[1] != layer.in_dim:

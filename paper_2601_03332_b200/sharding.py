@@ -24,7 +24,7 @@ import numpy as np
 from . import _capi
 from ._capi import lib
 from .lutkan import (ConfigError, DimensionError, Engine, KanLayerSpec, LutLayerArtifact, OobConfig, OobStats,
-                     QuantConfig, check, compile_layer)
+                     QuantConfig, _torch_enter, _torch_exit, check, compile_layer)
 
 
 ROW_ALIGN = 64  # csrc/lkg_internal.h kRowAlign: shard starts keep every row's lane phase
@@ -109,22 +109,50 @@ class ColumnShardedChain:
         import torch
         devs = [a.device(self.engine) for a in self.layers]
         handles = (C.c_void_p * len(devs))(*[d.handle for d in devs])
+        X = _cuda_input(X, self.layers[0].in_dim)
         rows = X.shape[0]
+        m_out = devs[-1].info.out_dim
         if Y is None:
-            Y = torch.empty((rows, devs[-1].info.out_dim), device=X.device, dtype=torch.float32)
+            Y = torch.empty((rows, m_out), device=X.device, dtype=torch.float32)
+        _check_output(Y, X, rows, m_out)
         stats = (_capi.OobStatsC * len(devs))()
+        ext = _torch_enter(self.engine, X)
         check(lib().lkg_model_forward_sharded(self.engine.handle, handles, len(devs), C.c_void_p(X.data_ptr()), rows,
                                               C.c_void_p(Y.data_ptr()), stats))
+        _torch_exit(ext, X, Y)
         return Y, [OobStats._from(s) for s in stats]
+
+
+def _cuda_input(X, in_dim: int):
+    """A CUDA [rows, in_dim] tensor as the contiguous fp32 the C-ABI reads (as lutkan._forward)."""
+    if not (type(X).__module__.startswith("torch") and X.is_cuda):
+        raise DimensionError("sharded forwards take CUDA tensors")
+    if X.dim() != 2 or X.shape[1] != in_dim:
+        raise DimensionError("batch column count does not match artifact in_dim")
+    return X.contiguous().float()
+
+
+def _check_output(Y, X, rows: int, cols: int) -> None:
+    import torch
+    if not (isinstance(Y, torch.Tensor) and Y.is_cuda and Y.device == X.device and Y.dtype == torch.float32
+            and Y.is_contiguous() and tuple(Y.shape) == (rows, cols)):
+        raise DimensionError(f"Y must be a contiguous float32 CUDA tensor of shape ({rows}, {cols}) on {X.device}")
 
 
 def layer_forward_blocked(art: LutLayerArtifact, X, x_blk: int, engine: Engine):
     """One layer on input in the rank-major all-gather layout (torch CUDA tensors)."""
     import torch
     d = art.device(engine)
+    if not (isinstance(X, torch.Tensor) and X.is_cuda):
+        raise DimensionError("layer_forward_blocked takes a CUDA tensor")
+    if x_blk <= 0 or art.in_dim % x_blk or X.numel() % art.in_dim:
+        raise DimensionError("blocked input: x_blk must divide in_dim and X must hold rows x in_dim values")
+    X = X.contiguous().float()
     rows = X.numel() // art.in_dim
     Y = torch.empty((rows, d.info.out_dim), device=X.device, dtype=torch.float32)
     st = _capi.OobStatsC()
+    ext = _torch_enter(engine, X)
     check(lib().lkg_layer_forward_blocked(engine.handle, d.handle, C.c_void_p(X.data_ptr()), rows, x_blk,
                                           C.c_void_p(Y.data_ptr()), C.byref(st)))
+    _torch_exit(ext, X, Y)
     return Y, OobStats._from(st)

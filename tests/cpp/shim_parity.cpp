@@ -10,6 +10,7 @@
 #include <fstream>
 #include <iterator>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "lutkan/artifact_io.hpp"
@@ -120,6 +121,42 @@ int main() {
       threw = true;
     }
     CHECK(threw, "non-finite input -> NonFiniteError");
+  }
+  // concurrency (test_spline.cpp:310-323 "batch forward is safe to call concurrently"):
+  // 4 host threads call the three batch entry points at once through their default contexts;
+  // every thread's results are bit-identical to a single-threaded call
+  {
+    QuantConfig cfg;
+    const KanLayerSpec layer = gen_sanity_layer(5);
+    const std::vector<KanLayerSpec> layers = {gen_layer(7, 10, 8, 8, 3), gen_layer(8, 8, 3, 8, 3)};
+    const LutLayerArtifact art = lutkan::compile_layer(layer, cfg, OobConfig{});
+    const auto chain = lutkan::compile_model(layers, cfg, OobConfig{});
+    Matrix X = gen_inputs(43, 4099, 10, -1.2, 1.2, false);
+    for (double& v : X.data) v = static_cast<double>(static_cast<float>(v));
+    const auto want_l = lutkan_b200::lut_layer_forward_batch(art, X, Tier::Optimized);
+    const auto want_m = lutkan_b200::lut_model_forward_batch(chain, X, Tier::Optimized);
+    const Matrix want_s = lutkan_b200::layer_forward_batch(layer, X, Tier::Optimized);
+    std::vector<int> ok(4, 0);
+    std::vector<std::thread> ts;
+    for (int t = 0; t < 4; ++t)
+      ts.emplace_back([&, t] {
+        int good = 1;
+        for (int it = 0; it < 25; it++) {  // interleave many calls per thread
+          const auto l = lutkan_b200::lut_layer_forward_batch(art, X, Tier::Optimized);
+          const auto m = lutkan_b200::lut_model_forward_batch(chain, X, Tier::Optimized);
+          const Matrix sp = lutkan_b200::layer_forward_batch(layer, X, Tier::Optimized);
+          good &= l.first.data == want_l.first.data && l.second.n_oob_inputs == want_l.second.n_oob_inputs &&
+                  l.second.n_oob_samples == want_l.second.n_oob_samples && l.second.n_samples == want_l.second.n_samples;
+          good &= m.Y.data == want_m.Y.data && m.per_layer.size() == want_m.per_layer.size() &&
+                  m.per_layer[0].n_oob_inputs == want_m.per_layer[0].n_oob_inputs &&
+                  m.per_layer[1].n_oob_inputs == want_m.per_layer[1].n_oob_inputs;
+          good &= sp.data == want_s.data;
+        }
+        ok[t] = good;
+      });
+    for (auto& t : ts) t.join();
+    CHECK(ok[0] && ok[1] && ok[2] && ok[3],
+          "4 threads x (lut_layer_forward_batch, lut_model_forward_batch, layer_forward_batch): bit-identical");
   }
   // eval_accuracy and the artifact container through the shim
   {

@@ -1,0 +1,93 @@
+"""Parity at the BENCHMARKED geometry (the largest parity runs had been 20k rows while
+the bench times 1M): configs[1] ("C2") at its full 1,000,000 rows in both quantization schemes, and
+configs[3] ("C4") layer launches at the full 1,048,576-row batch (the transposed-input walk over
+whole 1024-row tiles), against the reference CPU implementation (oracle/_ref) on all host threads.
+
+C2 (runtime.cpp:298-314): per layer within 1e-5 on the GPU's own fp32 layer input
+and OobStats exact over all 1M rows; argmax classes of the GPU chain vs the reference chain counted,
+each mismatch explained (oracle/agreement.py), none unexplained; and the LUT classifier vs the
+B-spline classifier it was compiled from (the paper's comparison) reported.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import assert_close, stats_list
+
+pytestmark = pytest.mark.gpu
+NT = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def c2_inputs(lk):
+    return lk.recipe_inputs(2, 0, 1_000_000)
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_c2_full_batch_parity_and_argmax(lk, oracle, c2_inputs, scheme):
+    import torch
+    from oracle.agreement import chain_agreement
+    X = c2_inputs
+    rows = X.shape[0]
+    specs = [lk.recipe_layer(2, l) for l in range(2)]
+    qc = lk.QuantConfig(64, lk.Scheme(scheme), lk.Dtype(scheme))
+    chain = lk.compile_model(specs, qc, lk.OobConfig())          # C2 contract: closed + clip_x
+    chain_o = [oracle.compile_layer(oracle.recipe_layer(2, l), 64, scheme, 1, 0, 1, 0) for l in range(2)]
+    for g, o in zip(chain, chain_o):
+        assert np.array_equal(g.q_table, o.q) and np.array_equal(g.scale.view(np.uint32), o.scale.view(np.uint32))
+    Xd = torch.from_numpy(X).cuda()
+    H, st0 = lk.lut_layer_forward_batch(chain[0], Xd)
+    Y, st1 = lk.lut_layer_forward_batch(chain[1], H)
+    r = lk.lut_model_forward_batch(chain, Xd)
+    assert torch.equal(r.Y, Y)                                   # the chain is exactly the two launches
+    H, Y = H.cpu().numpy(), Y.cpu().numpy()
+    X64 = X.astype(np.float64)
+    Ho, so0 = oracle.lut_forward(chain_o[0], X64, 1, NT)
+    assert_close(H, Ho, f"C2 layer 0 scheme {scheme}, 1M rows")
+    assert stats_list(st0) == [int(v) for v in so0]
+    Y1o, so1 = oracle.lut_forward(chain_o[1], H.astype(np.float64), 1, NT)
+    assert_close(Y, Y1o, f"C2 layer 1 (GPU hidden) scheme {scheme}, 1M rows")
+    assert stats_list(st1) == [int(v) for v in so1]
+    rep = chain_agreement(oracle, chain_o, X, [H], Y, NT)
+    print(f"C2 scheme {scheme}: argmax agreement {rep['agree']}/{rep['rows']} "
+          f"(near_tie {rep['near_tie']}, knot_straddle {rep['knot_straddle']}, unexplained {rep['unexplained']})")
+    assert rep["unexplained"] == 0, rep
+    # per-layer OobStats of the chain call equal the reference chain's
+    _, sto = oracle.lut_model_forward(chain_o, X64[:200000], 1, NT)
+    rs = lk.lut_model_forward_batch(chain, Xd[:200000])
+    assert [stats_list(s) for s in rs.per_layer] == sto.astype(int).tolist()
+    # the paper's classifier comparison: LUT vs the B-spline model it was compiled from
+    Ys = lk.layer_forward_batch(specs[1], lk.layer_forward_batch(specs[0], Xd))
+    agree_spline = float(np.mean(np.argmax(Ys.cpu().numpy(), 1) == np.argmax(Y, 1)))
+    print(f"C2 scheme {scheme}: LUT vs spline argmax agreement {agree_spline:.6f}")
+    assert agree_spline > 0.99
+
+
+def test_c4_full_batch_xt_rows(lk, oracle):
+    """C4 layer 0 (1024 -> 1024) and layer 1 (on the GPU's hidden values) launched on the full
+    1,048,576-row batch (XT walk, TMEM f64 accumulators), checked against the reference on 64-row
+    samples from the first, middle and last 1024-row tiles; layer 0's OOB counts over the whole
+    batch exact (in_range, runtime.cpp:71-75, evaluated on every input)."""
+    import torch
+    rows = 1_048_576
+    contract = (0, 0)                                           # half_open, clip_x
+    X = torch.from_numpy(lk.recipe_inputs(4, 0, rows)).cuda()
+    arts = [lk.compile_layer(lk.recipe_layer(4, l), lk.QuantConfig(64),
+                             lk.OobConfig(lk.BoundaryMode.HalfOpen, lk.OobPolicy.ClipX)) for l in range(2)]
+    H, st0 = lk.lut_layer_forward_batch(arts[0], X)
+    Y, st1 = lk.lut_layer_forward_batch(arts[1], H)
+    sample = np.concatenate([np.arange(0, 64), np.arange(rows // 2 - 32, rows // 2 + 32), np.arange(rows - 64, rows)])
+    idx = torch.from_numpy(sample).cuda()
+    Xs, Hs, Ys = X[idx].cpu().numpy(), H[idx].cpu().numpy(), Y[idx].cpu().numpy()
+    for l, (inp, out) in enumerate(((Xs, Hs), (Hs, Ys))):
+        ao = oracle.compile_layer(oracle.recipe_layer(4, l), 64, 0, 1, 0, *contract)
+        Yo, _ = oracle.lut_forward(ao, inp.astype(np.float64), 1, NT)
+        assert_close(out, Yo, f"C4 layer {l}, rows sampled from a 1,048,576-row launch")
+    # OOB counts of the full launches: every coordinate outside [t_0, t_K) (half_open) counted
+    for st, inp, a in ((st0, X, arts[0]), (st1, H, arts[1])):
+        lo, hi = float(a.knots[0]), float(a.knots[-1])
+        oob = ~((inp >= lo) & (inp < hi))
+        assert st.n_samples == rows and st.n_inputs == rows * inp.shape[1]
+        assert st.n_oob_inputs == int(oob.sum().item())
+        assert st.n_oob_samples == int(oob.any(dim=1).sum().item())

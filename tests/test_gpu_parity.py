@@ -677,6 +677,67 @@ def test_chain_graph_replay_matches_direct(lk):
 
 
 @pytest.mark.gpu
+def test_chain_graph_owns_its_buffers(lk):
+    """A captured graph keeps working after the same engine ran larger or wider forwards (which
+    grow, i.e. free and reallocate, the engine's scratch and transposed-input buffers): the graph
+    owns its own. Layer 0 (256 -> 256, 16 j-blocks, 1024-row batch) takes the XT walk,
+    whose tensor map is baked into the captured launch."""
+    import torch
+    eng = lk.Engine(0)
+    specs = [lk.gen_layer(21, 256, 256, 8), lk.gen_layer(22, 256, 4, 8)]
+    chain = lk.compile_model(specs, lk.QuantConfig(64), lk.OobConfig(), engine=eng)
+    X = torch.empty((1024, 256), device="cuda").uniform_(-1.2, 1.2)
+    want = lk.lut_model_forward_batch(chain, X, engine=eng).Y.clone()
+    Y = torch.empty((1024, 4), device="cuda")
+    g = lk.ChainGraph(chain, X, Y, engine=eng)
+    big = torch.empty((16384, 256), device="cuda").uniform_(-1.2, 1.2)
+    wide = [lk.compile_layer(lk.gen_layer(23, 256, 1024, 8), lk.QuantConfig(64), lk.OobConfig(), engine=eng),
+            lk.compile_layer(lk.gen_layer(24, 1024, 4, 8), lk.QuantConfig(64), lk.OobConfig(), engine=eng)]
+    for _ in range(2):
+        lk.lut_model_forward_batch(chain, big, engine=eng)   # scratch and xt grow (reallocated)
+        lk.lut_model_forward_batch(wide, big, engine=eng)
+        Y.zero_()
+        g()
+        torch.cuda.synchronize()
+        assert torch.equal(Y, want)
+    eng.collect(2)
+    del g
+
+
+@pytest.mark.gpu
+def test_torch_inputs_are_stream_ordered(lk):
+    """A torch input still being written on torch's current stream (delayed by a long-running
+    kernel) is read only after that write: the engine's private stream waits on torch's stream
+    (ADVICE r1), for the LUT chain, the spline forward and graph replay."""
+    import torch
+    eng = lk.Engine(0)
+    spec = lk.recipe_layer(3, 0)
+    a = lk.compile_layer(spec, lk.QuantConfig(64), lk.OobConfig(), engine=eng)
+    X2 = torch.from_numpy(lk.recipe_inputs(3, 0, 65536)).cuda()
+    want = lk.lut_layer_forward_batch(a, X2, engine=eng)[0].clone()
+    want_s = lk.layer_forward_batch(spec, X2, engine=eng).clone()
+    X = torch.zeros_like(X2)
+    for fn, ref in ((lambda: lk.lut_layer_forward_batch(a, X, engine=eng)[0], want),
+                    (lambda: lk.layer_forward_batch(spec, X, engine=eng), want_s)):
+        X.zero_()
+        torch.cuda.synchronize()
+        torch.cuda._sleep(200_000_000)   # ~0.1 s on torch's stream before the new batch lands
+        X.copy_(X2)
+        Y = fn()
+        assert torch.equal(Y, ref)
+    Y = torch.empty((65536, 64), device="cuda")
+    g = lk.ChainGraph([a], X, Y, engine=eng)
+    X.zero_()
+    torch.cuda.synchronize()
+    torch.cuda._sleep(200_000_000)
+    X.copy_(X2)
+    out = g()
+    assert torch.equal(out, want)
+    eng.collect(1)
+    del g
+
+
+@pytest.mark.gpu
 def test_balanced_rows_small_batches_bit_identical(lk, oracle):
     """One-j-block layers split any batch over every SM in 64-aligned row ranges: prefixes of a batch
     (1 .. 5000 rows, odd sizes, fewer rows than SMs x 64) reproduce the full launch bit for bit, and

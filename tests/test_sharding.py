@@ -185,6 +185,38 @@ def test_nccl_sharded_chain_row_chunks_overlap(tmp_path):
 
 
 @pytest.mark.gpu
+def test_nccl_sharded_chain_row_chunks_widening(tmp_path):
+    """Row-chunked column-sharded chain whose hidden width GROWS ([64, 32, 64, 48, 2]): chunk c
+    of every layer owns a fixed region of the scratch and gather buffers (sized by the widest
+    layer), so a wider layer l+1 never writes over layer l's chunks c+1.. while their gathers are
+    in flight on the communication stream (LKG_SHARD_CHUNKS=3, 1-rank NCCL). Equal bit for bit to
+    the unsharded chain, stats included."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "import paper_2601_03332_b200 as lk\n"
+        "from paper_2601_03332_b200.sharding import ColumnShardedChain\n"
+        "eng = lk.Engine(0); eng.init_nccl(lk.nccl_unique_id(), 1, 0)\n"
+        "dims = [64, 32, 64, 48, 2]\n"
+        "specs = [lk.gen_layer(11 + l, dims[l], dims[l + 1], 8) for l in range(4)]\n"
+        "chain = ColumnShardedChain.compile(specs, dims[1:], lk.QuantConfig(64), lk.OobConfig(), eng, 1, 0)\n"
+        "for rows in (70001, 9000):\n"
+        "    X = torch.empty((rows, 64), device='cuda').uniform_(-1.2, 1.2)\n"
+        "    for _ in range(3):\n"
+        "        Y, st = chain.forward(X)\n"
+        "        ref = lk.lut_model_forward_batch(chain.layers, X, engine=eng)\n"
+        "        assert torch.equal(Y, ref.Y), (Y - ref.Y).abs().max()\n"
+        "        assert [(s.n_oob_inputs, s.n_oob_samples) for s in st] == "
+        "[(s.n_oob_inputs, s.n_oob_samples) for s in ref.per_layer]\n"
+        "print('ok')\n") % root
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, LKG_SHARD_CHUNKS="3"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout[-2000:], r.stderr[-4000:])
+
+
+@pytest.mark.gpu
 def test_batch_shards_and_host_chunks_bit_identical(lk):
     """Batch shards (batch_bounds: 64-row aligned starts) and the host path's row chunks give
     every row exactly the bits of one whole-batch launch (bit-identical to 1 GPU)."""
