@@ -547,13 +547,13 @@ def _torch_enter(eng: Engine, t):
 
 
 def _torch_exit(ext, *tensors):
-    """Order torch's current stream after the engine's work, and keep the tensors the engine read
-    or wrote alive for the caching allocator until that work is done."""
+    """Order torch's current stream after the engine's work. The tensors the engine read or wrote
+    were allocated on that stream, so the caching allocator reuses their memory only after this
+    wait (record_stream on the engine's stream is deliberately NOT used: that stream may be
+    destroyed with its Engine before the allocator records the tensor's release on it)."""
     import torch
     dev = tensors[0].device
     torch.cuda.current_stream(dev).wait_stream(ext)
-    for t in tensors:
-        t.record_stream(ext)
 
 
 def _forward(chain, X, engine: Engine | None):
