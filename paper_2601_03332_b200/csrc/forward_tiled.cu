@@ -41,6 +41,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "coords.cuh"
 #include "lkg_internal.h"
@@ -58,7 +59,12 @@ constexpr int G = 8;                // inputs per line
 constexpr int JB = 16;              // outputs per line / j-block
 constexpr int LINE = G * JB;        // 128 bytes
 constexpr int PROW = 80;            // bytes per P/Q/CB row (16 floats + 16 B pad, conflict-free)
+constexpr int PLINE = 2 * LINE;     // IDP pair line: 8 inputs x 16 outputs x (code, next code)
 constexpr int kFlushBlocks = 1;     // f64 flush after every tile (8 inputs): partial sums stay short
+// IDP integer lerp: W0 + W1 = 2^15 (so W0*u0 + W1*u1 <= 2^15 * 255 < 2^23 stays a magic float's
+// mantissa), packed as the dp2a weight word W0 | W1 << 16 = 2^15 + 65535*W1, formed from the float
+// 2^23 + W1 by one IMAD with this bias (unsigned wrap-around intended)
+constexpr uint32_t kWordBias = 32768u - 0x4B000000u * 65535u;
 constexpr int kFp32MaxD = 256;      // fp32 accumulation bound
 
 struct TiledArgs {
@@ -102,6 +108,26 @@ __device__ __forceinline__ float magic(uint32_t w, uint32_t sel) {
   return __uint_as_float(__byte_perm(w, 0x4B000000u, sel));  // 2^23 + byte
 }
 
+// IDP.2A: a.h0 * b.byte(0|2) + a.h1 * b.byte(1|3) + c (16-bit x 8-bit, unsigned)
+__device__ __forceinline__ uint32_t dp2a_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("dp2a.lo.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t dp2a_hi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("dp2a.hi.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// Byte offset of (input il, output j, sample l or l+1) inside an IDP pair line: output pairs
+// (j, j+1) share a word [u_l(j), u_l+1(j), u_l(j+1), u_l+1(j+1)]; outputs 8h..8h+7 form a 16-byte
+// half stored at chunk h ^ (il >> 2) of the input's 32 bytes, so the 8 lanes of an LDS.128 phase
+// (8 distinct rotated inputs) hit 8 distinct 16-byte bank groups.
+__host__ __device__ __forceinline__ int pair_off(int il, int j, int next) {
+  return il * 32 + (((j >> 3) ^ (il >> 2)) << 4) + ((j & 7) >> 1) * 4 + (j & 1) * 2 + next;
+}
+
 // Item u -> (row tile, j-block). GC: row tiles fastest (every CTA in flight shares the current
 // tile in L2). Otherwise groups of a.rt_group row tiles sweep all j-blocks with the row tile
 // fastest: the group's x blocks stay in L2 across j-blocks and each tile is read once per group
@@ -120,7 +146,7 @@ __device__ __forceinline__ void item_coords(const TiledArgs& a, bool gc, uint32_
 }
 
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1, bool GC = false,
-          bool BAL = false, int XB = 1, bool XT = false>
+          bool BAL = false, int XB = 1, bool XT = false, int IDPM = 0>
 __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   // Two stage buffers, a compile-time count: NS as a runtime value turned every per-tile
@@ -333,7 +359,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
 #pragma unroll 1
       for (int s = 0; s < n_steps; s++) {
         const int il = (s + lane) & 7;
-        const uint8_t* Tq = Tcodes + il * JB;
+        const uint8_t* Tq = Tcodes + (IDPM == 1 ? pair_off(il, 0, 0) : il * JB);
         const uint8_t* Tp = T + a.p_off + il * PROW;
         float2 cb[8];
         if (SR) {
@@ -378,11 +404,6 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           nfacc = fmaf(x, 0.0f, nfacc);  // NaN once any input is NaN or inf
           oob_item += (uint32_t)!in;
           row_oob |= (uint32_t)(!in) << r;
-          const float w0 = 1.0f - w1;
-          const float cA = -fmaf(w0, M, OFF), cB = -w1 * M;
-          const uint8_t* qp = Tq + (k * L + l0) * LINE;
-          const uint4 c0 = GC ? gc_load(qp) : *reinterpret_cast<const uint4*>(qp);
-          const uint4 c1 = GC ? gc_load(qp + LINE) : *reinterpret_cast<const uint4*>(qp + LINE);
           const int prow = ((ZS && !in) ? K : k) * (G * PROW);  // zero block masks the table term
           const float4* pp = reinterpret_cast<const float4*>(Tp + prow);
           float bx = 0.0f;
@@ -390,8 +411,64 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
             const float xb = ZS ? x : xp;  // clip_x clips the base branch too (runtime.cpp:189)
             bx = lkg::silu_fast(xb);
           }
+          const float2 BX = make_float2(bx, bx);
+          if constexpr (IDPM != 0) {
+            // Integer lerp: W1 = round(w1 * 2^15), W0 = 2^15 - W1; one dp2a per output
+            // gives 2^23 + W0*u0 + W1*u1 exactly as a magic float, one FADD2 per output pair removes
+            // the magic (and the symmetric codes' +128 bias), P arrives pre-scaled by 2^-15.
+            const uint32_t Wd = __float_as_uint(fmaf(w1, 32768.0f, 8388608.0f)) * 65535u + kWordBias;
+            uint32_t wd[8];
+            if constexpr (IDPM == 1) {  // pair lines: the words are in shared memory as they are
+              const uint8_t* qp = Tq + (k * L + l0) * PLINE;
+              // Tq points at half 0 (chunk il >> 2 of the input's 32 bytes); half 1 is the other chunk
+              const uint4 h0 = *reinterpret_cast<const uint4*>(qp);
+              const uint4 h1 = *reinterpret_cast<const uint4*>(qp + 16 - ((il >> 2) << 5));
+              wd[0] = h0.x, wd[1] = h0.y, wd[2] = h0.z, wd[3] = h0.w, wd[4] = h1.x, wd[5] = h1.y, wd[6] = h1.z, wd[7] = h1.w;
+            } else {  // standard lines: pair each code with the next line's (one PRMT per 2 outputs)
+              const uint8_t* qp = Tq + (k * L + l0) * LINE;
+              const uint4 c0 = GC ? gc_load(qp) : *reinterpret_cast<const uint4*>(qp);
+              const uint4 c1 = GC ? gc_load(qp + LINE) : *reinterpret_cast<const uint4*>(qp + LINE);
+              const uint32_t u0[4] = {c0.x, c0.y, c0.z, c0.w}, u1[4] = {c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+              for (int q = 0; q < 4; q++) {
+                wd[2 * q] = __byte_perm(u0[q], u1[q], 0x5140);
+                wd[2 * q + 1] = __byte_perm(u0[q], u1[q], 0x7362);
+              }
+            }
+            constexpr float MOFF = ASYM ? -8388608.0f : -12582912.0f;  // -(2^23 [+ 128 * 2^15])
+            const float2 MO = make_float2(MOFF, MOFF);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+              const float4 P = pp[q];
+              const float2 Pl = make_float2(P.x, P.y), Ph = make_float2(P.z, P.w);
+              const float2 a01 = __fadd2_rn(make_float2(__uint_as_float(dp2a_lo(Wd, wd[2 * q], 0x4B000000u)),
+                                                        __uint_as_float(dp2a_hi(Wd, wd[2 * q], 0x4B000000u))), MO);
+              const float2 a23 = __fadd2_rn(make_float2(__uint_as_float(dp2a_lo(Wd, wd[2 * q + 1], 0x4B000000u)),
+                                                        __uint_as_float(dp2a_hi(Wd, wd[2 * q + 1], 0x4B000000u))), MO);
+              float2 s0 = acc[r][2 * q], s1 = acc[r][2 * q + 1];
+              s0 = __ffma2_rn(Pl, a01, s0);
+              s1 = __ffma2_rn(Ph, a23, s1);
+              if (SR) {
+                s0 = __ffma2_rn(cb[2 * q], BX, s0);
+                s1 = __ffma2_rn(cb[2 * q + 1], BX, s1);
+              }
+              if (ASYM) {
+                const float4 Q = reinterpret_cast<const float4*>(T + a.q_off + il * PROW + prow)[q];
+                s0 = __fadd2_rn(s0, make_float2(Q.x, Q.y));
+                s1 = __fadd2_rn(s1, make_float2(Q.z, Q.w));
+              }
+              acc[r][2 * q] = s0;
+              acc[r][2 * q + 1] = s1;
+            }
+            continue;
+          }
+          const float w0 = 1.0f - w1;
+          const float cA = -fmaf(w0, M, OFF), cB = -w1 * M;
+          const uint8_t* qp = Tq + (k * L + l0) * LINE;
+          const uint4 c0 = GC ? gc_load(qp) : *reinterpret_cast<const uint4*>(qp);
+          const uint4 c1 = GC ? gc_load(qp + LINE) : *reinterpret_cast<const uint4*>(qp + LINE);
           const float2 W0 = make_float2(w0, w0), W1 = make_float2(w1, w1);
-          const float2 CA = make_float2(cA, cA), CB = make_float2(cB, cB), BX = make_float2(bx, bx);
+          const float2 CA = make_float2(cA, cA), CB = make_float2(cB, cB);
           const uint32_t w0w[4] = {c0.x, c0.y, c0.z, c0.w}, w1w[4] = {c1.x, c1.y, c1.z, c1.w};
 #pragma unroll
           for (int q = 0; q < 4; q++) {
@@ -805,11 +882,12 @@ __global__ void build_small_kernel(const uint8_t* q, const float* scale, const f
     reinterpret_cast<float*>(lut + cb_off)[i * MP + j] = (float)((double)gains[2 * E + e] * (double)gains[e]);
 }
 
-// Reference layout -> tiles (one thread per (edge, segment) cell).
+// Reference layout -> tiles (one thread per (edge, segment) cell). idp: 1 = pair lines, 2 = standard
+// lines; both store P pre-scaled by 2^-15 (exact) for the integer lerp.
 __global__ void build_tiles_kernel(const uint8_t* q, const float* scale, const float* ymin, const float* gains,
                                    uint8_t* tiles, int64_t tile_bytes, int32_t n_ih, int32_t d, int32_t m,
                                    int32_t K, int32_t L, int32_t p_off, int32_t q_off, int32_t cb_off, int sym,
-                                   int sr, int asym) {
+                                   int sr, int asym, int idp) {
   const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t E = (int64_t)d * m;
   if (cell >= E * K) return;
@@ -819,20 +897,50 @@ __global__ void build_tiles_kernel(const uint8_t* q, const float* scale, const f
   const int ih = i / G, il = i % G, jb = j / JB, jl = j % JB;
   uint8_t* t = tiles + ((int64_t)jb * n_ih + ih) * tile_bytes;
   const uint8_t* src = q + cell * L;
-  for (int l = 0; l < L; l++) t[(k * L + l) * LINE + il * JB + jl] = sym ? (uint8_t)(src[l] ^ 0x80u) : src[l];
+  if (idp == 1) {
+    for (int l = 0; l < L; l++) {
+      uint8_t* line = t + (int64_t)(k * L + l) * PLINE;
+      line[pair_off(il, jl, 0)] = sym ? (uint8_t)(src[l] ^ 0x80u) : src[l];
+      line[pair_off(il, jl, 1)] = l + 1 < L ? (sym ? (uint8_t)(src[l + 1] ^ 0x80u) : src[l + 1]) : 0;
+    }
+  } else {
+    for (int l = 0; l < L; l++) t[(k * L + l) * LINE + il * JB + jl] = sym ? (uint8_t)(src[l] ^ 0x80u) : src[l];
+  }
   // fused gains in f64 (runtime.cpp:263-273), then one rounding to f32
   const double cs = sr ? (double)gains[2 * E + e] * (double)gains[E + e] : 1.0;
   float* P = reinterpret_cast<float*>(t + p_off + (k * G + il) * PROW) + jl;
-  *P = (float)(cs * (double)scale[cell]);
+  *P = (float)(cs * (double)scale[cell]) * (idp ? 0x1p-15f : 1.0f);
   if (asym) *reinterpret_cast<float*>(t + q_off + (k * G + il) * PROW + jl * 4) = (float)(cs * (double)ymin[cell]);
   if (sr && k == 0)
     *reinterpret_cast<float*>(t + cb_off + il * PROW + jl * 4) = (float)((double)gains[2 * E + e] * (double)gains[e]);
 }
 
+// Weight-rounding error of the integer lerp, per output column j: sum over inputs i of
+// (max_k |P_kij| * max_l |u_l+1 - u_l|)^2 (one thread per edge; f64 atomics). W1 = round(w1 2^15)
+// moves each interpolant by at most that product times 2^-16, independently per input.
+__global__ void idp_bound_kernel(const uint8_t* q, const float* scale, const float* gains, int32_t d, int32_t m,
+                                 int32_t K, int32_t L, int sr, int sym, double* acc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t E = (int64_t)d * m;
+  if (e >= E) return;
+  const double cs = sr ? std::fabs((double)gains[2 * E + e] * (double)gains[E + e]) : 1.0;
+  double worst = 0.0;
+  for (int k = 0; k < K; k++) {
+    const uint8_t* c = q + (e * K + k) * L;
+    int dq = 0;
+    for (int l = 0; l + 1 < L; l++) {
+      const int a0 = sym ? (int)(int8_t)c[l] : (int)c[l], a1 = sym ? (int)(int8_t)c[l + 1] : (int)c[l + 1];
+      dq = max(dq, abs(a1 - a0));
+    }
+    worst = fmax(worst, cs * std::fabs((double)scale[e * K + k]) * dq);
+  }
+  atomicAdd(acc + (e % m), worst * worst);
+}
+
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1, bool GC = false,
-          bool BAL = false, int XB = 1, bool XT = false>
+          bool BAL = false, int XB = 1, bool XT = false, int IDPM = 0>
 void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
-  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT>;
+  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, IDPM>;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -843,6 +951,24 @@ void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
   kern<<<grid, W * 32, smem, st>>>(a);
 }
 
+// The layer's table walk (TileGeom::idp) as a runtime choice over the compiled variants; pair lines
+// are never used with codes in global memory.
+template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1, bool GC = false,
+          bool BAL = false, int XB = 1, bool XT = false>
+void launch_idp(int idp, cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
+  if (idp == 2) {
+    launch_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, 2>(st, a, smem, grid);
+    return;
+  }
+  if constexpr (!GC) {
+    if (idp == 1) {
+      launch_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, 1>(st, a, smem, grid);
+      return;
+    }
+  }
+  launch_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, 0>(st, a, smem, grid);
+}
+
 }  // namespace
 
 namespace lkg {
@@ -850,6 +976,7 @@ namespace lkg {
 static constexpr int kW = 16, kR = 2;          // fp32 mode: 16 warps x 64 rows = 1024-row tiles
 static constexpr int kW64 = kW, kR64 = kR;      // f64 mode: same shape, f64 accumulators in TMEM
 static constexpr int kSmallMaxBytes = 200 * 1024;
+static constexpr double kIdpRss = 1.5e-6;  // IDP weight-rounding bound (build_tiles)
 
 bool tiled_eligible(const lkg_layer* L) {
   if (L->float_table.p || L->K > kMaxKT) return false;
@@ -914,20 +1041,49 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
       return;
     }
   }
-  int64_t off = (int64_t)(K * Ls + 1) * LINE;
-  gm.p_off = (int32_t)off;
-  off += (int64_t)(K + 1) * G * PROW;
-  if (asym) {
-    gm.q_off = (int32_t)off;
-    off += (int64_t)(K + 1) * G * PROW;
+  // Integer-lerp (IDP) walk when its weight rounding stays far inside the parity bar: the 2^-16
+  // weight error moves output j by a sum of independent terms whose root-sum-square is at most
+  // sqrt(sum_i e_ij^2) 2^-16 (idp_bound_kernel); allowed up to kIdpRss (a 6-sigma tail of that,
+  // plus the fp32 accumulation's ~1e-6, stays below 1e-5). LKG_IDP=0 forces the fp32 lerp.
+  static const char* idp_env = getenv("LKG_IDP");
+  int idp = 0;
+  if (!(idp_env && idp_env[0] == '0') && L->q.p) {
+    DBuf acc;
+    acc.alloc(sizeof(double) * m);
+    LKG_CUDA(cudaMemsetAsync(acc.p, 0, acc.bytes, ctx->stream));
+    const int64_t E = (int64_t)d * m;
+    idp_bound_kernel<<<(unsigned)((E + 255) / 256), 256, 0, ctx->stream>>>(
+        L->q.as<uint8_t>(), L->scale.as<float>(), L->gains.as<float>(), d, m, K, Ls, sr, !asym, acc.as<double>());
+    LKG_CUDA(cudaGetLastError());
+    ctx->launches++;
+    std::vector<double> h(m);
+    LKG_CUDA(cudaMemcpyAsync(h.data(), acc.p, acc.bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    double worst = 0.0;
+    for (double v : h) worst = std::max(worst, v);
+    gm.idp_rss = std::sqrt(worst) * 0x1p-16;
+    idp = gm.idp_rss <= kIdpRss ? 2 : 0;
   }
-  if (sr) {
-    gm.cb_off = (int32_t)off;
-    off += G * PROW;
-  }
-  off = (off + 127) / 128 * 128;
   const size_t xs_bytes = (size_t)1 * kW * G * (32 * kR + 4) * 4;  // one x buffer (fwd_tiled XB)
+  auto layout = [&](int mode) {  // tile offsets for the given code layout; returns the tile bytes
+    int64_t o = mode == 1 ? (int64_t)K * Ls * PLINE : (int64_t)(K * Ls + 1) * LINE;
+    gm.p_off = (int32_t)o;
+    o += (int64_t)(K + 1) * G * PROW;
+    if (asym) {
+      gm.q_off = (int32_t)o;
+      o += (int64_t)(K + 1) * G * PROW;
+    }
+    if (sr) {
+      gm.cb_off = (int32_t)o;
+      o += G * PROW;
+    }
+    return (o + 127) / 128 * 128;
+  };
   static const bool force_gc = getenv("LKG_FORCE_GC") != nullptr;  // test / tuning hook
+  // pair lines (twice the code bytes) when two stage buffers of them still fit shared memory
+  if (idp && !force_gc && 2 * layout(1) + xs_bytes + kMaxKT * 16 + 64 <= 227 * 1024) idp = 1;
+  int64_t off = layout(idp == 1 ? 1 : 0);
+  gm.idp = idp;
   gm.codes_global = force_gc || 2 * off + xs_bytes + kMaxKT * 16 + 64 > 227 * 1024;  // codes stay in global (L2)
   if (gm.codes_global && 2 * (off - gm.p_off) + xs_bytes + kMaxKT * 16 + 64 > 227 * 1024) return;  // generic
   gm.tile_bytes = off;
@@ -939,7 +1095,7 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   LKG_CUDA(cudaMemsetAsync(L->tiles.p, 0, L->tiles.bytes, ctx->stream));
   build_tiles_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(
       L->q.as<uint8_t>(), L->scale.as<float>(), L->ymin.as<float>(), L->gains.as<float>(), L->tiles.as<uint8_t>(),
-      off, gm.n_ih, d, m, K, Ls, gm.p_off, gm.q_off, gm.cb_off, !asym, sr, asym);
+      off, gm.n_ih, d, m, K, Ls, gm.p_off, gm.q_off, gm.cb_off, !asym, sr, asym, gm.idp);
   LKG_CUDA(cudaGetLastError());
   ctx->launches++;
   // Layers above 2 GB of codes (configs[3]/[4]) keep their codes only in the tiles; the reference
@@ -953,7 +1109,7 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
 
 // Tiles -> reference q layout for input rows [i0, i1) (inverse of build_tiles_kernel's code scatter).
 __global__ void tiles_to_q_kernel(const uint8_t* tiles, int64_t tile_bytes, int32_t n_ih, int32_t i0, int32_t i1,
-                                  int32_t m, int32_t K, int32_t L, int sym, uint8_t* q) {
+                                  int32_t m, int32_t K, int32_t L, int sym, int idp, uint8_t* q) {
   const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // cell within the chunk
   const int64_t n = (int64_t)(i1 - i0) * m * K;
   if (cell >= n) return;
@@ -962,7 +1118,8 @@ __global__ void tiles_to_q_kernel(const uint8_t* tiles, int64_t tile_bytes, int3
   const int i = i0 + (int)(e / m), j = (int)(e % m);
   const uint8_t* t = tiles + ((int64_t)(j / JB) * n_ih + i / G) * tile_bytes;
   for (int l = 0; l < L; l++) {
-    const uint8_t b = t[(k * L + l) * LINE + (i % G) * JB + (j % JB)];
+    const uint8_t b = idp == 1 ? t[(int64_t)(k * L + l) * PLINE + pair_off(i % G, j % JB, 0)]
+                               : t[(k * L + l) * LINE + (i % G) * JB + (j % JB)];
     q[cell * L + l] = sym ? (uint8_t)(b ^ 0x80u) : b;
   }
 }
@@ -980,7 +1137,7 @@ void download_q_from_tiles(lkg_ctx* ctx, const lkg_layer* L, uint8_t* host_q) {
     const int64_t cells = (int64_t)(i1 - i0) * m * L->K;
     tiles_to_q_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(
         L->tiles.as<uint8_t>(), gm.tile_bytes, gm.n_ih, i0, i1, m, L->K, L->L, L->scheme == LKG_SCHEME_SYMMETRIC,
-        tmp.as<uint8_t>());
+        gm.idp, tmp.as<uint8_t>());
     LKG_CUDA(cudaGetLastError());
     LKG_CUDA(cudaMemcpyAsync(host_q + (int64_t)i0 * row_bytes, tmp.p, (size_t)(i1 - i0) * row_bytes,
                              cudaMemcpyDeviceToHost, ctx->stream));
@@ -1219,14 +1376,14 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
 #define CASE(S)                                                                                                \
   case S:                                                                                                      \
     if (f64 && gm.codes_global)                                                                                \
-      launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, true, false, 1, true>(       \
-          ctx->stream, a, smem, grid);                                                                         \
+      launch_idp<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, true, false, 1, true>(       \
+          gm.idp, ctx->stream, a, smem, grid);                                                                         \
     else if (f64)                                                                                              \
-      launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, false, false, 1, true>(      \
-          ctx->stream, a, smem, grid);                                                                         \
+      launch_idp<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, false, false, 1, true>(      \
+          gm.idp, ctx->stream, a, smem, grid);                                                                         \
     else                                                                                                       \
-      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, false, 1, true>(         \
-          ctx->stream, a, smem, grid);                                                                         \
+      launch_idp<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, false, 1, true>(         \
+          gm.idp, ctx->stream, a, smem, grid);                                                                         \
     break;
       CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
@@ -1240,9 +1397,9 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
 #define CASE(S)                                                                                                \
   case S:                                                                                                      \
     if (f64)                                                                                                   \
-      launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, true>(ctx->stream, a, smem, grid); \
+      launch_idp<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, true>(gm.idp, ctx->stream, a, smem, grid); \
     else                                                                                                       \
-      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, true>(ctx->stream, a, smem, grid);    \
+      launch_idp<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, true>(gm.idp, ctx->stream, a, smem, grid);    \
     break;
       CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
@@ -1266,7 +1423,7 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
     smem += kMaxKT * 16 + ((g2.tile_bytes + 15) & ~15);
     switch (sel) {
 #define CASE(S) \
-  case S: launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, true, 1, false, true>(ctx->stream, a, smem, grid); break;
+  case S: launch_idp<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, true, 1, false, true>(gm.idp, ctx->stream, a, smem, grid); break;
       CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
     }
@@ -1282,15 +1439,15 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
 #define CASE(S)                                                                                         \
   case S:                                                                                               \
     if (f64)                                                                                            \
-      launch_tiled<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true>(ctx->stream, a, smem, grid);     \
+      launch_idp<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true>(gm.idp, ctx->stream, a, smem, grid);     \
     else if (xb2)                                                                                       \
-      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, true,              \
-                   ((S >> 2) & 1) ? 1 : 2>(ctx->stream, a, smem, grid);                                 \
+      launch_idp<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, true,              \
+                   ((S >> 2) & 1) ? 1 : 2>(gm.idp, ctx->stream, a, smem, grid);                                 \
     else if (bal)                                                                                       \
-      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, true>(ctx->stream, a, \
+      launch_idp<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, true>(gm.idp, ctx->stream, a, \
                                                                                          smem, grid);  \
     else                                                                                                \
-      launch_tiled<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false>(ctx->stream, a, smem, grid);        \
+      launch_idp<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false>(gm.idp, ctx->stream, a, smem, grid);        \
     break;
     CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE

@@ -71,6 +71,11 @@ struct TileGeom {
   int32_t p_stride = 0;  // bytes between (k, i_lo) rows of the P block
   int32_t small = 0, MP = 0;  // whole-layer-in-smem layout (m <= 8), MP = padded out_dim
   int32_t codes_global = 0;   // tiled layout whose code block is read from global/L2 (GC kernel)
+  // Integer-lerp table walk (forward_tiled.cu, IDP): 0 = fp32 magic-float lerp; 1 = pair lines
+  // (each code stored next to its successor: one dp2a per output, no byte extraction); 2 = the
+  // standard lines, pairs built with one PRMT per 2 outputs. P is stored pre-scaled by 2^-15.
+  int32_t idp = 0;
+  double idp_rss = 0.0;       // statistical bound of the 2^-16 weight-rounding error (build_tiles)
 };
 
 }  // namespace lkg

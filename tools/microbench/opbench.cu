@@ -147,6 +147,107 @@ __global__ void k_lds(float* out, long long* cyc) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// dp2a (IDP.2A): two 16-bit x 8-bit products + 32-bit accumulate, the integer lerp of the
+// IDP table walk (forward_tiled.cu): lo and hi halves of the code word
+__device__ __forceinline__ uint32_t dp2a_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm volatile("dp2a.lo.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t dp2a_hi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm volatile("dp2a.hi.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+__global__ void k_dp2a(uint32_t seed, float* out, long long* cyc) {
+  uint32_t v[CHAINS], w = seed * 7u;
+  for (int c = 0; c < CHAINS; c++) v[c] = seed + c;
+  long long t0 = clock64();
+  for (int it = 0; it < NITER; it++) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; c++) { v[c] = dp2a_lo(w, v[c], seed); v[c] = dp2a_hi(w, v[c], seed); }
+  }
+  long long t1 = clock64();
+  uint32_t s = 0; for (int c = 0; c < CHAINS; c++) s += v[c];
+  if (s == 12345u) out[0] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+__global__ void k_imad(uint32_t seed, float* out, long long* cyc) {
+  uint32_t v[CHAINS], w = seed * 7u;
+  for (int c = 0; c < CHAINS; c++) v[c] = seed + c;
+  long long t0 = clock64();
+  for (int it = 0; it < NITER; it++) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; c++) { v[c] = v[c] * w + seed; v[c] = v[c] * seed + w; }
+  }
+  long long t1 = clock64();
+  uint32_t s = 0; for (int c = 0; c < CHAINS; c++) s += v[c];
+  if (s == 12345u) out[0] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+// the IDP walk's core per 2 outputs: 2 dp2a (lo, hi) -> FADD2 (magic off) -> FFMA2 (x P) -> FFMA2 (base)
+// 5 issue slots; counted as 5 ops per pair
+__global__ void k_idp_core(uint32_t seed, float* out, long long* cyc) {
+  unsigned long long acc[CHAINS];
+  uint32_t v[CHAINS], w = seed * 7u;
+  float2 pp = make_float2(1e-3f, 2e-3f), cb = make_float2(0.5f, 0.25f), bx = make_float2(0.1f, 0.1f);
+  const float2 mg = make_float2(-12582912.f, -12582912.f);
+  for (int c = 0; c < CHAINS; c++) { v[c] = seed + 3 * c; acc[c] = 0; }
+  long long t0 = clock64();
+  for (int it = 0; it < NITER; it++) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; c++) {
+      const uint32_t r0 = dp2a_lo(w, v[c], 0x4B000000u), r1 = dp2a_hi(w, v[c], 0x4B000000u);
+      float2 f = make_float2(__uint_as_float(r0), __uint_as_float(r1));
+      f = __fadd2_rn(f, mg);
+      float2 a = *(float2*)&acc[c];
+      a = __ffma2_rn(pp, f, a);
+      a = __ffma2_rn(cb, bx, a);
+      acc[c] = *(unsigned long long*)&a;
+      v[c] += 0x01010101u;
+    }
+  }
+  long long t1 = clock64();
+  float s = 0; for (int c = 0; c < CHAINS; c++) { float2 t = *(float2*)&acc[c]; s += t.x + t.y; }
+  if (s == 1.2345f) out[0] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+// the round-1 core per 2 outputs: 4 PRMT + 5 FFMA2 (9 issue slots), counted as 9 ops per pair
+__global__ void k_prmt_core(uint32_t seed, float* out, long long* cyc) {
+  unsigned long long acc[CHAINS];
+  uint32_t v[CHAINS], u[CHAINS];
+  const float2 W0 = make_float2(0.3f, 0.3f), W1 = make_float2(0.7f, 0.7f), CA = make_float2(-3e6f, -3e6f),
+               CB2 = make_float2(-5e6f, -5e6f), pp = make_float2(1e-3f, 2e-3f), cb = make_float2(0.5f, 0.25f),
+               bx = make_float2(0.1f, 0.1f);
+  for (int c = 0; c < CHAINS; c++) { v[c] = seed + 3 * c; u[c] = seed * 5 + c; acc[c] = 0; }
+  long long t0 = clock64();
+  for (int it = 0; it < NITER; it++) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; c++) {
+      const float2 fa = make_float2(__uint_as_float(__byte_perm(v[c], 0x4B000000u, 0x7440)),
+                                    __uint_as_float(__byte_perm(v[c], 0x4B000000u, 0x7441)));
+      const float2 fb = make_float2(__uint_as_float(__byte_perm(u[c], 0x4B000000u, 0x7440)),
+                                    __uint_as_float(__byte_perm(u[c], 0x4B000000u, 0x7441)));
+      const float2 a0 = __ffma2_rn(W0, fa, CA), b0 = __ffma2_rn(W1, fb, CB2);
+      float2 a = *(float2*)&acc[c];
+      a = __ffma2_rn(pp, a0, a);
+      a = __ffma2_rn(pp, b0, a);
+      a = __ffma2_rn(cb, bx, a);
+      acc[c] = *(unsigned long long*)&a;
+      v[c] += 0x01010101u;
+      u[c] += 0x01010101u;
+    }
+  }
+  long long t1 = clock64();
+  float s = 0; for (int c = 0; c < CHAINS; c++) { float2 t = *(float2*)&acc[c]; s += t.x + t.y; }
+  if (s == 1.2345f) out[0] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 template <typename K, typename... A>
 void run(const char* name, K kern, int grid, int block, double ops_per_thread_iter, A... args) {
   long long* cyc; float* out;
@@ -182,6 +283,10 @@ int main() {
     run("ffma", k_ffma, g, 256, CHAINS * 2.0, 1.0001f);
     run("ffma2(x2)", k_ffma2, g, 256, CHAINS * 4.0, 1.0001f);
     run("prmt", k_prmt, g, 256, CHAINS * 2.0, 12345u);
+    run("dp2a", k_dp2a, g, 256, CHAINS * 2.0, 12345u);
+    run("imad", k_imad, g, 256, CHAINS * 2.0, 12345u);
+    run("idp_core(5/pair)", k_idp_core, g, 256, CHAINS * 5.0, 12345u);
+    run("prmt_core(9/pair)", k_prmt_core, g, 256, CHAINS * 9.0, 12345u);
     run("dadd", k_dadd, g, 256, CHAINS * 2.0, 1.0001);
     run("f2f64+dadd", k_f2f64, g, 256, CHAINS * 1.0, 1.0001f);
     run("lds32", k_lds<4>, g, 256, 1.0);
