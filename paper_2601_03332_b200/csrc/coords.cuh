@@ -73,6 +73,12 @@ __device__ __forceinline__ float silu_fast(float x) {
   return x * r;
 }
 
+// silu(x) = x / (1 + exp(-x)) evaluated in f64 (spline.cpp:105-108) and rounded once to f32.
+__device__ __forceinline__ float silu_exact(float x) {
+  const double xd = x;
+  return (float)(xd / (1.0 + exp(-xd)));
+}
+
 // Fast path of lut_coords for the table walk: the segment from the uniform-grid estimate, with no
 // knot compares, and z from that segment's constants. An estimate can only be off by one within a
 // few fp32 roundings of a knot, where z lands next to a sample node; every coordinate closer than

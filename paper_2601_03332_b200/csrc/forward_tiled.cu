@@ -93,6 +93,9 @@ struct TiledArgs {
   // XT mode: the layer input was transposed to [d][rows] (launch_forward_tiled) and each warp's x
   // block [8 inputs][64 rows] is one 2D TMA box of this map
   alignas(64) CUtensorMap xmap;
+  // ... and the layer's base-branch activations silu(x') of the same input, [d][rows] (computed
+  // once per input element by the transpose pass, in f64: correctly rounded to f32)
+  alignas(64) CUtensorMap smap;
 };
 
 using lkg::bulk_g2s;
@@ -168,8 +171,10 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   // XB x-tile buffers per warp. One (the next block staged after the steps, from L1 mostly) leaves
   // 35 KB more L1 than two (staged a tile ahead): measured C4 -7%, C3 -5%, C5 -4%, C2a -2%; only the
   // int8 one-j-block layer (configs[1]) is faster with two (+2%).
-  float* xsw = reinterpret_cast<float*>(smem + NS * sb) + warp * XB * G * XS;
-  float4* ktab = reinterpret_cast<float4*>(smem + NS * sb + XB * W * G * XS * 4);
+  // XT: each x buffer is followed by its silu box (the base branch reads it instead of silu(x'))
+  constexpr int XW = XT ? 2 : 1;
+  float* xsw = reinterpret_cast<float*>(smem + NS * sb) + warp * XB * G * XS * XW;
+  float4* ktab = reinterpret_cast<float4*>(smem + NS * sb + XB * W * G * XS * XW * 4);
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + kMaxKT);
   uint32_t* fin = reinterpret_cast<uint32_t*>(full + 4);  // warps done with each stage buffer
   uint64_t* xbar = full + 8;  // XT: per-warp x-block barriers (W <= 16)
@@ -262,13 +267,18 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   };
   uint32_t xphase = 0;
   auto stage_x = [&](int64_t r0_, int ih_, int buf) {
-    if constexpr (XT) {  // one 2D TMA box [8 inputs][64 rows] of the transposed input
+    if constexpr (XT) {  // 2D TMA boxes [8 inputs][64 rows] of the transposed input and its silu
       if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the warp's reads, then TMA writes
-        mbar_expect_tx(&xbar[warp], (uint32_t)(G * ROWS_W * 4));
+        mbar_expect_tx(&xbar[warp], (uint32_t)(2 * G * ROWS_W * 4));
+        float* dst = xsw + buf * G * XS * XW;
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-            ::"r"(lkg::smem_u32(xsw + buf * G * XS)), "l"(&a.xmap), "r"((int)r0_), "r"(ih_ * G),
+            ::"r"(lkg::smem_u32(dst)), "l"(&a.xmap), "r"((int)r0_), "r"(ih_ * G), "r"(lkg::smem_u32(&xbar[warp]))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+            ::"r"(lkg::smem_u32(dst + G * XS)), "l"(&a.smap), "r"((int)r0_), "r"(ih_ * G),
             "r"(lkg::smem_u32(&xbar[warp]))
             : "memory");
       }
@@ -341,7 +351,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
         asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       __syncwarp();
-      const float* xs = xsw + (XB == 2 ? xbuf * G * XS : 0);
+      const float* xs = xsw + (XB == 2 ? xbuf * G * XS * XW : 0);
       if constexpr (XB == 2) {
         if (ih + 1 < a.n_ih)
           stage_x(row0, ih + 1, xbuf ^ 1);
@@ -361,16 +371,6 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
         const int il = (s + lane) & 7;
         const uint8_t* Tq = Tcodes + (IDPM == 1 ? pair_off(il, 0, 0) : il * JB);
         const uint8_t* Tp = T + a.p_off + il * PROW;
-        float2 cb[8];
-        if (SR) {
-          const float4* cbp = reinterpret_cast<const float4*>(T + a.cb_off + il * PROW);
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const float4 v = cbp[q];
-            cb[2 * q] = make_float2(v.x, v.y);
-            cb[2 * q + 1] = make_float2(v.z, v.w);
-          }
-        }
         // ---- steps 1-4 (runtime.cpp:170-190): mask, clip, segment, coordinates (coords.cuh),
         // the R rows' fast chains side by side, then the exact path once for any that need it
         float xv[R];
@@ -406,12 +406,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           row_oob |= (uint32_t)(!in) << r;
           const int prow = ((ZS && !in) ? K : k) * (G * PROW);  // zero block masks the table term
           const float4* pp = reinterpret_cast<const float4*>(Tp + prow);
-          float bx = 0.0f;
-          if (SR) {
-            const float xb = ZS ? x : xp;  // clip_x clips the base branch too (runtime.cpp:189)
-            bx = lkg::silu_fast(xb);
-          }
-          const float2 BX = make_float2(bx, bx);
+          (void)xp;
           if constexpr (IDPM != 0) {
             // Integer lerp: W1 = round(w1 * 2^15), W0 = 2^15 - W1; one dp2a per output
             // gives 2^23 + W0*u0 + W1*u1 exactly as a magic float, one FADD2 per output pair removes
@@ -448,10 +443,6 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
               float2 s0 = acc[r][2 * q], s1 = acc[r][2 * q + 1];
               s0 = __ffma2_rn(Pl, a01, s0);
               s1 = __ffma2_rn(Ph, a23, s1);
-              if (SR) {
-                s0 = __ffma2_rn(cb[2 * q], BX, s0);
-                s1 = __ffma2_rn(cb[2 * q + 1], BX, s1);
-              }
               if (ASYM) {
                 const float4 Q = reinterpret_cast<const float4*>(T + a.q_off + il * PROW + prow)[q];
                 s0 = __fadd2_rn(s0, make_float2(Q.x, Q.y));
@@ -485,10 +476,6 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
             s1 = __ffma2_rn(Ph, a1, s1);
             s0 = __ffma2_rn(Pl, b0, s0);
             s1 = __ffma2_rn(Ph, b1, s1);
-            if (SR) {
-              s0 = __ffma2_rn(cb[2 * q], BX, s0);
-              s1 = __ffma2_rn(cb[2 * q + 1], BX, s1);
-            }
             if (ASYM) {
               const float4 Q = reinterpret_cast<const float4*>(T + a.q_off + il * PROW + prow)[q];
               s0 = __fadd2_rn(s0, make_float2(Q.x, Q.y));
@@ -496,6 +483,37 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
             }
             acc[r][2 * q] = s0;
             acc[r][2 * q + 1] = s1;
+          }
+        }
+        if (SR) {
+          // base branch sum_i cb_ij silu(x'_i) (runtime.cpp:189,206-212) in a lane-UNIFORM input
+          // order (input s at step s): every lane reads the same CB row, so each LDS.128 is one
+          // broadcast wavefront instead of four rotated ones; the x value comes from the tile again
+          const float4* cbp = reinterpret_cast<const float4*>(T + a.cb_off + s * PROW);
+          float2 cbu[8];
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const float4 v = cbp[q];
+            cbu[2 * q] = make_float2(v.x, v.y);
+            cbu[2 * q + 1] = make_float2(v.z, v.w);
+          }
+#pragma unroll
+          for (int r = 0; r < R; r++) {
+            float bx;
+            if constexpr (XT) {
+              bx = xs[G * XS + s * XS + lane + 32 * r];  // the transpose pass's silu(x') box
+            } else {
+              const float xr = xs[s * XS + lane + 32 * r];
+              // clip_x clips the base branch too (runtime.cpp:189); zero_spline keeps the raw input
+              const float xb = ZS ? xr : fminf(fmaxf(xr, a.cc.lo), a.cc.hi_clip);
+              // long reductions (d > 256, f64 accumulators) take silu correctly rounded: the MUFU
+              // approximation's ~2^-22 relative error, summed over thousands of inputs, reaches the
+              // 1e-5 bar on configs[4]
+              bx = F64 ? lkg::silu_exact(xb) : lkg::silu_fast(xb);
+            }
+            const float2 BX = make_float2(bx, bx);
+#pragma unroll
+            for (int q = 0; q < 8; q++) acc[r][q] = __ffma2_rn(cbu[q], BX, acc[r][q]);
           }
         }
       }
@@ -1080,8 +1098,11 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
     return (o + 127) / 128 * 128;
   };
   static const bool force_gc = getenv("LKG_FORCE_GC") != nullptr;  // test / tuning hook
-  // pair lines (twice the code bytes) when two stage buffers of them still fit shared memory
-  if (idp && !force_gc && 2 * layout(1) + xs_bytes + kMaxKT * 16 + 64 <= 227 * 1024) idp = 1;
+  // Pair lines (twice the code bytes, no PRMT) only on request (LKG_IDP=1) and where two stage
+  // buffers of them fit: measured on configs[1] layer 0 they lose to the standard lines (0.496 vs
+  // 0.446 ms), which leave room for the second x buffer and halve the TMA bytes per tile.
+  if (idp && idp_env && idp_env[0] == '1' && !force_gc && 2 * layout(1) + xs_bytes + kMaxKT * 16 + 64 <= 227 * 1024)
+    idp = 1;
   int64_t off = layout(idp == 1 ? 1 : 0);
   gm.idp = idp;
   gm.codes_global = force_gc || 2 * off + xs_bytes + kMaxKT * 16 + 64 > 227 * 1024;  // codes stay in global (L2)
@@ -1269,8 +1290,11 @@ bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
   return tiled_smem(L1, kW, kR) + kMaxKT * 16 + ((g2.tile_bytes + 15) & ~15) <= 227 * 1024;
 }
 
-// X [rows][d] -> Xt [d][rows] (32x32 tiles through shared memory, both sides coalesced).
-__global__ void transpose_kernel(const float* __restrict__ X, int64_t rows, int32_t d, float* __restrict__ Xt) {
+// X [rows][d] -> Xt [d][rows] (32x32 tiles through shared memory, both sides coalesced), and the
+// base-branch activations St = silu(zs ? x : clamp(x, t_0, hi_clip)) in the same layout (f64, one
+// rounding to f32: each element once, instead of once per j-block inside the table walk).
+__global__ void transpose_kernel(const float* __restrict__ X, int64_t rows, int32_t d, float* __restrict__ Xt,
+                                 float* __restrict__ St, float lo, float hi_clip, int zs) {
   __shared__ float t[32][33];
   const int64_t r0 = (int64_t)blockIdx.x * 32;
   const int c0 = blockIdx.y * 32;
@@ -1283,7 +1307,11 @@ __global__ void transpose_kernel(const float* __restrict__ X, int64_t rows, int3
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int c = c0 + k;
     const int64_t r = r0 + threadIdx.x;
-    if (r < rows && c < d) Xt[(int64_t)c * rows + r] = t[threadIdx.x][k];
+    if (r < rows && c < d) {
+      const float v = t[threadIdx.x][k];
+      Xt[(int64_t)c * rows + r] = v;
+      St[(int64_t)c * rows + r] = lkg::silu_exact(zs ? v : fminf(fmaxf(v, lo), hi_clip));
+    }
   }
 }
 
@@ -1364,14 +1392,18 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   const bool xt = !(xt_env && xt_env[0] == '0') && (!gm.codes_global || xt_gc_ok) && !L2 && gm.n_jb >= 16 &&
                   x_blk <= 0 && rows % row_tile == 0 && L->in_dim % G == 0 && rows < (1ll << 31);
   if (xt) {
-    if (ctx->xt.bytes < sizeof(float) * (size_t)rows * L->in_dim) ctx->xt.alloc(sizeof(float) * (size_t)rows * L->in_dim);
+    const size_t xt_elems = (size_t)rows * L->in_dim;
+    if (ctx->xt.bytes < 2 * sizeof(float) * xt_elems) ctx->xt.alloc(2 * sizeof(float) * xt_elems);
     float* Xt = ctx->xt.as<float>();
+    float* St = Xt + xt_elems;
     transpose_kernel<<<dim3((unsigned)((rows + 31) / 32), (unsigned)((L->in_dim + 31) / 32)), dim3(32, 8), 0,
-                       ctx->stream>>>(X, rows, L->in_dim, Xt);
+                       ctx->stream>>>(X, rows, L->in_dim, Xt, St, a.cc.lo, a.cc.hi_clip, zs);
     LKG_CUDA(cudaGetLastError());
     ctx->launches++;
     encode_x_map(&a.xmap, Xt, rows, L->in_dim, 32 * R, G);
+    encode_x_map(&a.smap, St, rows, L->in_dim, 32 * R, G);
     a.X = Xt;
+    smem += (size_t)W * G * (32 * R) * 4;  // the silu boxes
     switch (sel) {
 #define CASE(S)                                                                                                \
   case S:                                                                                                      \

@@ -64,6 +64,15 @@ def main():
         top = sorted(((a[c], c) for c in STALLS), reverse=True)[:3]
         out.append(f"{op} | {s / total:.3f} | {a['Instructions Executed']} | " +
                    " ".join(f"{c[6:]}={v / total:.3f}" for v, c in top if v))
+    # shared-memory excess wavefronts (bank conflicts) by SASS line, where the source page has them
+    exc = [c for c in sh if "Shared Excessive" in c or ("Excessive" in c and "Shared" in c)]
+    for c in exc[:2]:
+        rows = sorted(data, key=lambda r: -val(r, c))[:8]
+        if rows and val(rows[0], c):
+            out.append(f"# top SASS lines by '{c}': address | value | source")
+            for r in rows:
+                if val(r, c):
+                    out.append(f"{r[si.get('Address', 0)]} | {val(r, c)} | {r[si['Source']].strip()[:90]}")
     print("\n".join(out))
 
 
