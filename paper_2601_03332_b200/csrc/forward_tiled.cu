@@ -402,8 +402,10 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           const int k = co.k, l0 = co.l0;
           const float xp = co.xp, w1 = co.w1;  // w1: multiple of 2^-23 -> exact magic constants
           nfacc = fmaf(x, 0.0f, nfacc);  // NaN once any input is NaN or inf
-          oob_item += (uint32_t)!in;
-          row_oob |= (uint32_t)(!in) << r;
+          if (!in) {  // (predicated adds: cheaper than materialising the flag)
+            oob_item++;
+            row_oob |= 1u << r;
+          }
           const int prow = ((ZS && !in) ? K : k) * (G * PROW);  // zero block masks the table term
           const float4* pp = reinterpret_cast<const float4*>(Tp + prow);
           (void)xp;
@@ -991,7 +993,13 @@ void launch_idp(int idp, cudaStream_t st, const TiledArgs& a, size_t smem, int g
 
 namespace lkg {
 
-static constexpr int kW = 16, kR = 2;          // fp32 mode: 16 warps x 64 rows = 1024-row tiles
+#ifndef LKG_W
+#define LKG_W 16
+#endif
+#ifndef LKG_R
+#define LKG_R 2
+#endif
+static constexpr int kW = LKG_W, kR = LKG_R;    // fp32 mode: 16 warps x 64 rows = 1024-row tiles
 static constexpr int kW64 = kW, kR64 = kR;      // f64 mode: same shape, f64 accumulators in TMEM
 static constexpr int kSmallMaxBytes = 200 * 1024;
 static constexpr double kIdpRss = 1.5e-6;  // IDP weight-rounding bound (build_tiles)
