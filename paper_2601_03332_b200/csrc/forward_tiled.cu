@@ -52,6 +52,26 @@
 #define LKG_NS 2  // fwd_tiled stage buffers (see the kernel)
 #endif
 
+// LKG_CHECKS builds (tools/gpu/checks.sh) compile device-side bounds assertions into the table
+// walks: every shared-memory table index, staged-tile address, TMEM column and output coordinate is
+// checked against its allocation and the kernel traps with a message on the first violation.
+// (compute-sanitizer is closed on the GPU pool; these asserts plus canary buffers and repeat-launch
+// bit-identity tests are the memory/race evidence.)
+#ifdef LKG_CHECKS
+#define LKG_DCHECK(cond, what)                                                                          \
+  do {                                                                                                  \
+    if (!(cond)) {                                                                                      \
+      printf("LKG_CHECKS %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, threadIdx.x, \
+             what);                                                                                     \
+      __trap();                                                                                         \
+    }                                                                                                   \
+  } while (0)
+#else
+#define LKG_DCHECK(cond, what) \
+  do {                         \
+  } while (0)
+#endif
+
 namespace {
 
 using lkg::kMaxKT;
@@ -69,7 +89,7 @@ constexpr int kFp32MaxD = 256;      // fp32 accumulation bound (SURVEY Appendix 
 
 struct TiledArgs {
   const uint8_t* tiles;
-  int64_t tile_bytes;
+  int64_t tile_bytes, tiles_bytes;  // one tile; the whole layer (bounds checks)
   int32_t n_ih, n_jb;
   int32_t p_off, q_off, cb_off;
   const float* X;
@@ -85,7 +105,7 @@ struct TiledArgs {
   // fused next layer (FUSE): a small-out_dim layer evaluated in the epilogue from the 16 hidden
   // activations each lane holds (the whole-layer "small" layout, resident in shared memory)
   const uint8_t* lut2;
-  int32_t lut2_bytes, p_off2, q_off2, cb_off2, MP2, m2;
+  int32_t lut2_bytes, p_off2, q_off2, cb_off2, MP2, m2, vp2;  // vp2: pair value table (small layout)
   float* Y2;
   unsigned long long* counters2;
   lkg::CoordConst cc2;
@@ -207,6 +227,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   if (F64) lkg::tmem_fence_after_sync();
   const uint32_t tm_base = F64 ? *tm_base_s : 0u;
   const uint32_t tm_warp = tm_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * R * 32);
+  LKG_DCHECK(!F64 || (uint32_t)((warp >> 2) * R * 32 + R * 32) <= kTmCols, "TMEM columns past the allocation");
 
   // Balanced rows (one j-block, e.g. configs[1] layer 0): CTA b owns rows [r_lo, r_hi) of an equal
   // split (starts at multiples of 64 rows, so every row keeps its lane and rotation and its result
@@ -408,6 +429,13 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           }
           const int prow = ((ZS && !in) ? K : k) * (G * PROW);  // zero block masks the table term
           const float4* pp = reinterpret_cast<const float4*>(Tp + prow);
+          LKG_DCHECK(k >= 0 && k < K && l0 >= 0 && l0 < L, "segment / sample index out of range");
+          LKG_DCHECK(prow >= 0 && prow <= K * G * PROW, "P row out of the staged block");
+          LKG_DCHECK(GC || (int64_t)(k * L + l0 + 1) * (IDPM == 1 ? PLINE : LINE) + LINE <= a.p_off,
+                     "code line past the staged code block");
+          LKG_DCHECK(!GC || ((int64_t)jb * a.n_ih + ih) * tb + (int64_t)(k * L + l0 + 2) * LINE <= a.tiles_bytes,
+                     "code line past the layer's tiles (GC)");
+          LKG_DCHECK(st >= 0 && st < NS, "stage index");
           (void)xp;
           if constexpr (IDPM != 0) {
             // Integer lerp: W1 = round(w1 * 2^15), W0 = 2^15 - W1; one dp2a per output
@@ -492,6 +520,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           // order (input s at step s): every lane reads the same CB row, so each LDS.128 is one
           // broadcast wavefront instead of four rotated ones; the x value comes from the tile again
           const float4* cbp = reinterpret_cast<const float4*>(T + a.cb_off + s * PROW);
+          LKG_DCHECK(a.cb_off + (s + 1) * PROW <= tb, "CB row past the tile");
           float2 cbu[8];
 #pragma unroll
           for (int q = 0; q < 4; q++) {
@@ -609,8 +638,10 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
                 if (t == 0 || has1) {
                   const int ii = i2 + t;
                   const bool tab = !(ZS && !c.in);
-                  const int cell = ii * K2 + c.k, l1 = min(c.l0 + 1, L2 - 1);
-                  const float2 v0 = V2[cell * L2 + c.l0], v1 = V2[cell * L2 + l1];
+                  // value table entry (k, l0, ii) of the interleaved small layout (build_small_vt_kernel)
+                  const int ent = (c.k * L2 + c.l0) * a.m + ii;
+                  const float2 v0 = V2[ent * (a.vp2 ? 2 : 1)];
+                  const float2 v1 = a.vp2 ? V2[ent * 2 + 1] : V2[ent + a.m];
                   const float w1 = c.w1, w0 = 1.0f - w1;
                   float2 v = tab ? make_float2(fmaf(w1, v1.x, w0 * v0.x), fmaf(w1, v1.y, w0 * v0.y))
                                  : make_float2(0.f, 0.f);
@@ -630,6 +661,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           oob2_rows += (uint32_t)r_oob2;
         } else {
           float* yr = a.Y + row * a.m + j0;
+          LKG_DCHECK(row >= 0 && row < a.rows && j0 < a.m, "output coordinate out of range");
           if (j0 + 16 <= a.m && (a.m & 3) == 0) {
 #pragma unroll
             for (int q = 0; q < 4; q++)
@@ -718,7 +750,7 @@ __device__ __forceinline__ void lkg_small_load(const float* p, float (&v)[N]) {
   }
 }
 
-template <bool ASYM, bool SR, bool ZS, bool VT, int MPT>
+template <bool ASYM, bool SR, bool ZS, bool VT, int MPT, bool VP = false>
 __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* lut = smem;
@@ -767,11 +799,20 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
       const float w1 = co.w1, w0 = 1.0f - w1;
       const float* CB = CBt + i * MP;
       if (VT) {
-        // V1 is the next line: l0 = L-1 comes with w1 = 0, and the table ends with a padding line
-        const float* V0 = V + (cell * L + co.l0) * MPT;
+        // Interleaved value table V[k][l][i] (input fastest, build_small_vt_kernel): the lanes of a
+        // load phase walk different inputs (i = lane + t mod d), so their entries sit in distinct
+        // bank groups whatever (k, l0) each row selects. VP: each entry also holds the next
+        // sample's values (one load); otherwise the next sample is the next line (+d entries).
+        // l0 = L-1 comes with w1 = 0, and the table ends with a padding line.
+        constexpr int ES = VP ? 2 * MPT : MPT;
+        const float* V0 = V + ((int64_t)(co.k * L + co.l0) * d + i) * ES;
+        LKG_DCHECK(co.k >= 0 && co.k < K && co.l0 >= 0 && co.l0 < L && i >= 0 && i < d, "value-table index");
+        LKG_DCHECK((VP ? ((int64_t)(co.k * L + co.l0) * d + i + 1) * ES
+                       : ((int64_t)(co.k * L + co.l0 + 1) * d + i + 1) * ES) * 4 <= a.cb_off,
+                   "value-table entry past the table");
         float v0[MPT], v1[MPT], cb[MPT];
         lkg_small_load<MPT>(V0, v0);
-        lkg_small_load<MPT>(V0 + MPT, v1);
+        lkg_small_load<MPT>(VP ? V0 + MPT : V0 + d * ES, v1);
         if (SR) lkg_small_load<MPT>(CB, cb);
 #pragma unroll
         for (int j = 0; j < MPT; j++) {
@@ -807,7 +848,7 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
       }
       return xrow + i;
     };
-    if (pairs) {
+    if (pairs && !VT) {
       // inputs in pairs (i even): one 8-byte load, both fast coordinate chains side by side,
       // the exact path once if either needs it
       // the next pair's load is issued one iteration ahead (its latency was the top stall)
@@ -829,6 +870,40 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
         accum(i, xx.x, c0);
         accum(i + 1, xx.y, c1);
       }
+    } else if (VT) {
+      // the interleaved value table wants consecutive lanes on consecutive inputs: lane walks
+      // i0, i0+1, ... (mod d) two inputs per iteration (two independent coordinate chains), the
+      // next pair's x loads one iteration ahead
+      auto nxt = [&](int v) { return v + 1 == d ? 0 : v + 1; };
+      int i = i0;
+      float xa_n = lo, xb_n = lo;
+      if (vrow) {
+        xa_n = __ldg(x_ptr(i));
+        if (d > 1) xb_n = __ldg(x_ptr(nxt(i)));
+      }
+      for (int t = 0; t < d; t += 2) {
+        const int ia = i, ib = nxt(i);
+        const float xa = xa_n, xb = xb_n;
+        i = nxt(ib);
+        if (vrow && t + 2 < d) {
+          xa_n = __ldg(x_ptr(i));
+          if (t + 3 < d) xb_n = __ldg(x_ptr(nxt(i)));
+        }
+        const bool two = t + 1 < d;
+        bool s0, s1;
+        lkg::Coord c0 = lkg::lut_coords_fast_nb(a.cc, ktab, xa, s0);
+        lkg::Coord c1 = lkg::lut_coords_fast_nb(a.cc, ktab, two ? xb : lo, s1);
+        if (s0 || s1) {
+          if (s0) c0 = lkg::lut_coords(a.cc, ktab, xa);
+          if (s1) c1 = lkg::lut_coords(a.cc, ktab, xb);
+        }
+        nfacc = fmaf(xa, 0.0f, nfacc);  // NaN once any input is NaN or inf
+        accum(ia, xa, c0);
+        if (two) {
+          nfacc = fmaf(xb, 0.0f, nfacc);
+          accum(ib, xb, c1);
+        }
+      }
     } else {
       int i = i0;
       float xn = lo;
@@ -843,6 +918,7 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
     }
     if (vrow) {
       float* yr = a.Y + row * a.m;
+      LKG_DCHECK(row >= 0 && row < a.rows, "small-layer output row out of range");
 #pragma unroll
       for (int j = 0; j < 8; j++)
         if (j < a.m) yr[j] = y[j];
@@ -864,9 +940,11 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
 
 // Dequantized value table for small layers: V[i][k][l][j] = (f32)(cs * (y_min + scale * q)),
 // cs = out*spline (1 for phi), evaluated in f64 like fetch_quant (runtime.cpp:124-128, 202-205).
+// Layout: entry (k, l, i) at ((k*L + l)*d + i) * ES floats, ES = MP (vp = 0) or 2*MP (vp = 1: the
+// entry also holds sample l+1's values; sample L-1 repeats its own).
 __global__ void build_small_vt_kernel(const uint8_t* q, const float* scale, const float* ymin, const float* gains,
                                       float* V, int32_t d, int32_t m, int32_t K, int32_t L, int32_t MP,
-                                      int32_t cb_off, int sr, int sym) {
+                                      int32_t cb_off, int sr, int sym, int vp) {
   const int64_t cell = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t E = (int64_t)d * m;
   if (cell >= E * K) return;
@@ -875,10 +953,17 @@ __global__ void build_small_vt_kernel(const uint8_t* q, const float* scale, cons
   const int i = (int)(e / m), j = (int)(e - (int64_t)i * m);
   const double cs = sr ? (double)gains[2 * E + e] * (double)gains[E + e] : 1.0;
   const double ym = ymin[cell], sc = scale[cell];
+  const int ES = vp ? 2 * MP : MP;
   for (int l = 0; l < L; l++) {
     const uint8_t b = q[cell * L + l];
     const double qv = sym ? (double)(int8_t)b : (double)b;
-    V[((int64_t)(i * K + k) * L + l) * MP + j] = (float)(cs * (ym + sc * qv));
+    const float v = (float)(cs * (ym + sc * qv));
+    float* ent = V + ((int64_t)(k * L + l) * d + i) * ES;
+    ent[j] = v;
+    if (vp) {
+      if (l > 0) ent[j - (int64_t)d * ES + MP] = v;  // the previous sample's "next" slot
+      if (l == L - 1) ent[MP + j] = v;
+    }
   }
   if (sr && k == 0)
     reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(V) + cb_off)[i * MP + j] =
@@ -1029,18 +1114,26 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
     const int MP = m <= 1 ? 1 : (m <= 2 ? 2 : (m <= 4 ? 4 : 8));
     // preferred: dequantized value table V = out*spline*(y_min + scale*q) in f32 (one rounding of
     // the f64 product), so the table walk is two loads and two FMAs per edge
-    const int64_t vt = ((int64_t)(d * K * Ls + 1) * MP * 4 + 15) / 16 * 16;  // + one padding line
+    // interleaved V[k][l][i] (conflict-free lane walk), with the next sample in each entry when
+    // that still fits (vp, one load per edge), else a padding line for the next-line read
+    int vp = 1;
+    int64_t vt = (int64_t)K * Ls * d * 2 * MP * 4;
+    if (vt + ((int64_t)d * MP * 4 + 15) / 16 * 16 + kMaxKT * 16 > kSmallMaxBytes) {
+      vp = 0;
+      vt = ((int64_t)(K * Ls + 1) * d * MP * 4 + 15) / 16 * 16;
+    }
     const int64_t vt_total = vt + ((int64_t)d * MP * 4 + 15) / 16 * 16;
     if (vt_total + kMaxKT * 16 <= kSmallMaxBytes) {
       gm.small = 2;
       gm.MP = MP;
+      gm.p_off = vp;  // (small == 2: p_off carries the pair flag)
       gm.cb_off = (int32_t)vt;
       gm.tile_bytes = vt_total;
       L->tiles.alloc((size_t)vt_total);
       LKG_CUDA(cudaMemsetAsync(L->tiles.p, 0, L->tiles.bytes, ctx->stream));
       build_small_vt_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, ctx->stream>>>(
           L->q.as<uint8_t>(), L->scale.as<float>(), L->ymin.as<float>(), L->gains.as<float>(),
-          L->tiles.as<float>(), d, m, K, Ls, MP, gm.cb_off, sr, !asym);
+          L->tiles.as<float>(), d, m, K, Ls, MP, gm.cb_off, sr, !asym, vp);
       LKG_CUDA(cudaGetLastError());
       ctx->launches++;
       return;
@@ -1221,9 +1314,9 @@ static int sm_count(int dev) {
   return sms[dev] > 0 ? sms[dev] : 148;
 }
 
-template <bool ASYM, bool SR, bool ZS, bool VT, int MPT>
+template <bool ASYM, bool SR, bool ZS, bool VT, int MPT, bool VP = false>
 static void launch_small_t(cudaStream_t st, const SmallArgs& a, size_t smem, int grid) {
-  auto kern = fwd_small<ASYM, SR, ZS, VT, MPT>;
+  auto kern = fwd_small<ASYM, SR, ZS, VT, MPT, VP>;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -1256,13 +1349,18 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
   const bool asym = L->scheme == LKG_SCHEME_ASYMMETRIC, sr = L->value_repr == LKG_REPR_SPLINE_COMPONENT;
   const bool zs = L->oob_policy == LKG_OOB_ZERO_SPLINE;
   const int sz = (sr << 1) | (int)zs;
-  if (gm.small == 2) {  // value table: compile-time padded out_dim
+  if (gm.small == 2) {  // value table: compile-time padded out_dim, pair entries or not
     const int mp = gm.MP == 1 ? 0 : (gm.MP == 2 ? 1 : (gm.MP == 4 ? 2 : 3));
-    switch ((mp << 2) | sz) {
-#define CASE(S) \
-  case S: launch_small_t<false, (S >> 1) & 1, S & 1, true, 1 << (S >> 2)>(ctx->stream, a, smem, grid); break;
+    switch ((gm.p_off << 4) | (mp << 2) | sz) {
+#define CASE(S)                                                                                                  \
+  case S:                                                                                                        \
+    launch_small_t<false, (S >> 1) & 1, S & 1, true, 1 << ((S >> 2) & 3), ((S >> 4) & 1) != 0>(ctx->stream, a, \
+                                                                                               smem, grid);     \
+    break;
       CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
       CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
+      CASE(16) CASE(17) CASE(18) CASE(19) CASE(20) CASE(21) CASE(22) CASE(23)
+      CASE(24) CASE(25) CASE(26) CASE(27) CASE(28) CASE(29) CASE(30) CASE(31)
 #undef CASE
     }
   } else {
@@ -1353,6 +1451,7 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   TiledArgs a{};
   a.tiles = L->tiles.as<uint8_t>();
   a.tile_bytes = gm.tile_bytes;
+  a.tiles_bytes = (int64_t)L->tiles.bytes;
   a.n_ih = gm.n_ih;
   a.n_jb = gm.n_jb;
   a.p_off = gm.p_off;
@@ -1456,6 +1555,7 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
     a.q_off2 = g2.q_off;
     a.cb_off2 = g2.cb_off;
     a.MP2 = g2.MP;
+    a.vp2 = g2.p_off;
     a.m2 = L2->col1 - L2->col0;
     a.Y2 = Y2;
     a.counters2 = ctx->counters.as<unsigned long long>() + 4 * (slot + 1);
