@@ -110,6 +110,8 @@ struct lkg_spec {
   lkg::DBuf coeffs32;  // f32 [i][R][j] transposed for the spline forward
   lkg::DBuf gains32;   // f32 [2][E]: out*base, out*spline
   lkg::DBuf spline_tiles;  // spline_tiled.cu layout (uniform cubic grids), built lazily
+  lkg::DBuf tc_b;          // spline_tc.cu: the coefficient matrix in UMMA blocks (hi/lo tf32), lazily
+  int32_t tc_n_ch = 0;
   int64_t sp_tile_bytes = 0;
   int32_t sp_n_ih = 0, sp_n_jb = 0;
 };
@@ -175,6 +177,7 @@ void launch_quantize(lkg_ctx* ctx, const double* v, int64_t nseg, int L, int asy
 void launch_eval(lkg_ctx* ctx, const lkg_spec* S, const lkg_layer* L, const void* X, bool x_f64, int64_t rows,
                  double* dsum, unsigned long long* u);
 bool launch_spline_tiled(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows, float* Y);
+bool launch_spline_tc(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows, float* Y);
 
 // Host model_gen (model_gen.cpp).
 int recipe_dims(int cfg, int* n_layers, int* dims, int* G, double* lo, double* hi);

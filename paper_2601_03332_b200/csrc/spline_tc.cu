@@ -1,0 +1,503 @@
+// spline_tc.cu — K3 on the 5th-generation tensor cores: the B-spline forward (the paper's "honest
+// baseline", layer_forward_batch -> forward_optimized, proj/core/src/spline.cpp:145-187) as a dense
+// GEMM with tcgen05.mma (kind::tf32, 3xTF32 split, fp32 accumulation in Tensor Memory).
+//
+//   y[s, j] = sum_i sum_r B_r(x_si) * C'_{i,r,j} + sum_i silu(x_si) * CB_{i,j}
+//           = A[s, (i,f)] * Bm[(i,f), j]       (feature f < R: basis value, f == R: silu, rest 0)
+//
+//  * Uniform knots, degree 3 (every BASELINE grid): the 4 non-zero basis values are the uniform
+//    cubic B-spline polynomials of u = frac((x - T_0)/h) (spline.cpp:69-83 in closed form, as the
+//    SIMT kernel spline_tiled.cu); silu(x) of the unclipped input (spline.cpp:105-108; the float
+//    model has no OOB handling, spline.cpp:165).
+//  * A (features) is produced in registers by 16 warps — four sets of four, one input of each chunk
+//    per set; thread t of a set owns row t of a 128-row tile and TMEM lane t — and written straight
+//    into Tensor Memory (tcgen05.st), split hi + lo (both round-to-nearest tf32): the MMA reads A
+//    from TMEM ("TS" form), no shared-memory round trip.
+//  * Bm is laid out once per spec (build_spline_tc) in the canonical K-major no-swizzle UMMA layout,
+//    one contiguous block per (n-tile, chunk of IC inputs) holding hi then lo; a producer warp
+//    streams the blocks through a 4-stage shared-memory ring with cp.async.bulk + mbarriers.
+//  * One elected thread issues, per 8 K-columns, A_hi*B_hi + A_hi*B_lo + A_lo*B_hi into a 128 x N
+//    fp32 accumulator in TMEM (products exact, dropped A_lo*B_lo ~ 2^-24 relative) and commits
+//    completion to mbarriers (tcgen05.commit). Double-buffered A and D.
+//  * Accumulation: the tensor cores round each MMA's addition into the fp32 accumulator one-sidedly
+//    (~0.5 ulp of |D| per MMA, measured), so D (double-buffered) holds one chunk (3 x KC/8 MMAs) and
+//    each feature set adds its N/4 columns of it into round-to-nearest fp32 registers, one chunk
+//    behind the MMAs (unbiased chunk-to-chunk sums).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+
+#include "coords.cuh"
+#include "lkg_internal.h"
+#include "tma.cuh"
+
+namespace {
+
+constexpr int TM = 128;        // rows per tile (UMMA M, one TMEM lane each)
+constexpr int NSB = 4;         // B stages
+constexpr int NFS = 4;         // feature-warp sets (4 warps = 128 rows each)
+constexpr int PF = 6;          // chunks of x prefetched per feature thread
+
+struct TcArgs {
+  const float* X;
+  int64_t rows;
+  int32_t d;
+  float* Y;
+  int32_t m;
+  const uint8_t* B;   // [n_nt][n_ch] blocks of 2 * N * KC floats (hi, lo)
+  int32_t n_nt, n_ch, IC, R, n0, gch;  // gch: chunks per accumulation (1)
+  float t0, inv_h;
+  int64_t n_rt, n_items;
+  uint32_t idesc;
+  int32_t dbg;  // experiment hook (LKG_TC_DBG): 1 = no MMAs, 2 = no feature math
+};
+
+__device__ __forceinline__ uint32_t rna_tf32(float v) {  // round-to-nearest tf32 (low 13 bits zero)
+  return (__float_as_uint(v) + 0x1000u) & 0xFFFFE000u;
+}
+
+__device__ __forceinline__ void tm_st8(uint32_t ta, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tm_st4(uint32_t ta, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ta), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+               "r"(v[3])
+               : "memory");
+}
+__device__ __forceinline__ void tm_st1(uint32_t ta, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(ta), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tm_st2(uint32_t ta, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(ta), "r"(v[0]), "r"(v[1]) : "memory");
+}
+template <int W>
+__device__ __forceinline__ void tm_stw(uint32_t ta, const uint32_t* v) {
+  if constexpr (W == 8) tm_st8(ta, v);
+  else if constexpr (W == 4) tm_st4(ta, v);
+  else tm_st2(ta, v);
+}
+__device__ __forceinline__ void tm_ld8(uint32_t ta, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(ta)
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld4(uint32_t ta, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(ta)
+               : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(lkg::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   lkg::smem_u32(bar))
+               : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem desc], kind::tf32, M = 128
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// K-major, no-swizzle canonical layout: core matrices of 8 rows x 16 B; LBO = next 16-B K chunk
+// (128 B away), SBO = next 8-row group (KC/4 * 128 B away).
+__device__ __forceinline__ uint64_t b_desc(uint32_t saddr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((128u >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm_100)
+  return d;                // base offset 0, legacy LBO mode, SWIZZLE_NONE
+}
+
+template <int N, int FP>
+__global__ void __launch_bounds__(32 * (4 * NFS + 2), 1) spline_tc(const __grid_constant__ TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int IC = FP <= 16 ? 4 : 2, KC = IC * FP;  // K columns per chunk (multiple of 8)
+  static_assert(KC % 8 == 0, "chunk must be whole K=8 MMA steps");
+  constexpr uint32_t kBlock = 2u * N * KC * 4u;       // hi + lo bytes per (n-tile, chunk)
+  constexpr int NA = 8 * KC + 2 * N <= 512 ? 4 : 2;    // A buffers (hi + lo each) in TMEM
+  constexpr uint32_t kCols = NA * 2 * KC + 2 * N;       // A buffers, D (2 buffers)
+  constexpr uint32_t kAlloc = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
+  static_assert(kCols <= 512, "TMEM budget");
+  constexpr uint32_t A0 = 0, D0 = NA * 2 * KC;  // TMEM column map
+  constexpr int CPS = N / NFS;             // accumulator columns per feature-warp set
+  constexpr int kFeat = 4 * NFS;           // feature warps
+  uint8_t* bst = smem;                     // NSB * kBlock
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NSB * kBlock);
+  uint64_t *b_full = bar, *b_empty = bar + NSB, *a_full = bar + 2 * NSB, *a_empty = a_full + NA,
+           *d_full = a_empty + NA, *d_empty = d_full + 2;
+  uint32_t* tm_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
+  // per-thread placement scratch: the input's FP features (hi row, then lo row), 2*FPP+4 words per
+  // thread (an odd number of 16-B units: the dense LDS.128 read-back is conflict-free)
+  constexpr int FPP = (FP + 3) / 4 * 4, SCR = 2 * FPP + 4;
+  uint32_t* scr = reinterpret_cast<uint32_t*>(smem + NSB * kBlock + 1024) + threadIdx.x * SCR;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < NSB; s++) {
+      lkg::mbar_init(&b_full[s], 1);
+      lkg::mbar_init(&b_empty[s], 1);
+    }
+    for (int s = 0; s < NA; s++) {
+      lkg::mbar_init(&a_full[s], 32 * kFeat);
+      lkg::mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < 2; s++) {
+      lkg::mbar_init(&d_full[s], 1);
+      lkg::mbar_init(&d_empty[s], 32 * kFeat);
+    }
+    lkg::mbar_fence_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(lkg::smem_u32(tm_slot)),
+                 "r"(kAlloc)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  const uint32_t tmem = *tm_slot;
+  const int64_t n_local = a.n_items > blockIdx.x ? (a.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int nch = a.n_ch;
+
+  if (warp == kFeat) {
+    // ---------------- producer: Bm blocks of this CTA's items, in order, through the ring
+    if (lane == 0) {
+      uint32_t q = 0;
+      for (int64_t li = 0; li < n_local; li++) {
+        const int64_t item = blockIdx.x + li * gridDim.x;
+        const int nt = (int)(item / a.n_rt);
+        const uint8_t* src = a.B + (int64_t)nt * nch * kBlock;
+        for (int c = 0; c < nch; c++, q++) {
+          const int s = q % NSB;
+          lkg::mbar_wait(&b_empty[s], ((q / NSB) & 1u) ^ 1u);
+          lkg::mbar_expect_tx(&b_full[s], kBlock);
+          lkg::bulk_g2s(bst + s * kBlock, src + (int64_t)c * kBlock, kBlock, &b_full[s]);
+        }
+      }
+    }
+  } else if (warp == kFeat + 1) {
+    // ---------------- MMA issuer: one thread; each chunk into a fresh D buffer
+    if (lane == 0) {
+      constexpr uint32_t sbo = (KC / 4) * 128;
+      uint32_t q = 0;
+      for (int64_t li = 0; li < n_local; li++) {
+        for (int c = 0; c < nch; c++, q++) {
+          const uint32_t db = q & 1u, ab = q % NA, s = q % NSB;
+          lkg::mbar_wait(&d_empty[db], ((q >> 1) & 1u) ^ 1u);  // the feature warps drained D[db]
+          lkg::mbar_wait(&a_full[ab], (q / NA) & 1u);
+          lkg::mbar_wait(&b_full[s], (q / NSB) & 1u);
+          tm_fence_after();
+          const uint32_t a_hi = tmem + A0 + ab * 2 * KC, a_lo = a_hi + KC, d_t = tmem + D0 + db * N;
+          const uint32_t bhi = lkg::smem_u32(bst + s * kBlock), blo = bhi + N * KC * 4;
+#pragma unroll
+          for (int ks = 0; ks < KC / 8; ks++) {
+            if (a.dbg & 1) break;
+            umma_tf32(d_t, a_hi + 8 * ks, b_desc(bhi + ks * 256, sbo), a.idesc, ks == 0 ? 0u : 1u);
+            umma_tf32(d_t, a_hi + 8 * ks, b_desc(blo + ks * 256, sbo), a.idesc, 1u);
+            umma_tf32(d_t, a_lo + 8 * ks, b_desc(bhi + ks * 256, sbo), a.idesc, 1u);
+          }
+          umma_commit(&b_empty[s]);
+          umma_commit(&a_empty[ab]);
+          umma_commit(&d_full[db]);
+        }
+      }
+    }
+  } else {
+    // ---------------- feature warps: 4 sets of 4 warps; thread = row of the tile = TMEM lane.
+    // Set fs writes the features of input fs of each chunk, and accumulates output columns
+    // [fs*CPS, (fs+1)*CPS) of the chunk results in fp32 registers (round-to-nearest adds, so the
+    // chunk-to-chunk sum stays unbiased), one chunk behind the MMAs.
+    const int fs = warp >> 2, quad = warp & 3;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const int row_in_tile = quad * 32 + lane;
+    double acc[CPS];  // f64: the chunk partials carry the tensor cores' one-sided rounding; their
+                      // sum over hundreds of chunks must not add a second one (fp32: 1.06x the bar on C4)
+    uint32_t q = 0;
+    int bq[NA];  // window column of this thread's input in each A buffer's last use
+#pragma unroll
+    for (int p = 0; p < NA; p++) bq[p] = 0;
+    for (int w = 0; w < SCR; w++) scr[w] = 0u;  // the placement scratch starts zeroed
+    auto drain = [&](uint32_t qq) {  // chunk qq's D into acc
+      const uint32_t db = qq & 1u;
+      lkg::mbar_wait(&d_full[db], (qq >> 1) & 1u);
+      tm_fence_after();
+      uint32_t dv[CPS];
+      if constexpr (CPS == 4) {
+        tm_ld4(tmem + lane_base + D0 + db * N + fs * CPS, dv);
+      } else {
+#pragma unroll
+        for (int c8 = 0; c8 < CPS / 8; c8++) tm_ld8(tmem + lane_base + D0 + db * N + fs * CPS + 8 * c8, dv + 8 * c8);
+      }
+      tm_wait_ld();
+      tm_fence_before();
+      mbar_arrive(&d_empty[db]);
+#pragma unroll
+      for (int n = 0; n < CPS; n++) acc[n] += (double)__uint_as_float(dv[n]);
+    };
+    for (int64_t li = 0; li < n_local; li++) {
+      const int64_t item = blockIdx.x + li * gridDim.x;
+      const int64_t rt = item % a.n_rt;
+      const int nt = (int)(item / a.n_rt);
+      const int64_t row = rt * TM + row_in_tile;
+      const bool vrow = row < a.rows;
+      const float* xr = a.X + (vrow ? row : 0) * a.d;
+#pragma unroll
+      for (int n = 0; n < CPS; n++) acc[n] = 0.0;
+      // x of this thread's row for the next PF chunks in flight (the row's inputs are strided by
+      // IC across chunks and each load is one 32-B sector per lane: without the prefetch every
+      // chunk waited a full L2/DRAM round trip)
+      float xq[PF];
+#pragma unroll
+      for (int p = 0; p < PF; p++) {
+        const int i = p * IC + fs;
+        xq[p] = (vrow && fs < IC && p < nch && i < a.d) ? __ldg(xr + i) : 0.0f;
+      }
+      for (int c = 0; c < nch; c++, q++) {
+        const uint32_t ab = q % NA;
+        const float x = xq[0];
+#pragma unroll
+        for (int p = 0; p + 1 < PF; p++) xq[p] = xq[p + 1];
+        {
+          const int i = (c + PF) * IC + fs;
+          xq[PF - 1] = (vrow && fs < IC && c + PF < nch && i < a.d) ? __ldg(xr + i) : 0.0f;
+        }
+        lkg::mbar_wait(&a_empty[ab], ((q / NA) & 1u) ^ 1u);
+        tm_fence_after();
+        const int base_old = bq[NA - 1];  // the scratch row's current window (last chunk's)
+#pragma unroll
+        for (int p = 0; p + 1 < NA; p++) bq[p] = bq[p + 1];
+        if (fs < IC && !(a.dbg & 2)) {
+          // uniform cubic B-spline basis at x (spline.cpp:69-83 in closed form): 4 values at basis
+          // indices r0..r0+3, as a 4-column window clamped inside the input's R basis columns
+          const float tt = (x - a.t0) * a.inv_h;
+          const float fl = floorf(tt);
+          const int mu = (int)fl;
+          const bool inside = tt >= 0.0f && mu < a.n0;  // false for NaN
+          const float u = tt - fl, om = 1.0f - u, u2 = u * u, u3 = u2 * u, s6 = 1.0f / 6.0f;
+          const float b0 = om * om * om * s6, b1 = fmaf(3.0f, u3, fmaf(-6.0f, u2, 4.0f)) * s6,
+                      b2 = fmaf(-3.0f, u3, fmaf(3.0f, u2, fmaf(3.0f, u, 1.0f))) * s6, b3 = u3 * s6;
+          const int r0 = mu - 3;
+          const int base = min(max(r0, 0), a.R - 4);
+          const int sh = inside ? base - r0 : 100;  // window column t holds basis value t + sh
+          uint32_t wh[4], wl[4];
+#pragma unroll
+          for (int t = 0; t < 4; t++) {
+            const int idx = t + sh;
+            const float v = idx == 0 ? b0 : idx == 1 ? b1 : idx == 2 ? b2 : idx == 3 ? b3 : 0.0f;
+            wh[t] = rna_tf32(v);
+            wl[t] = rna_tf32(v - __uint_as_float(wh[t]));
+          }
+          const float sx = lkg::silu_fast(x);  // silu of the unclipped input (as spline_tiled.cu)
+          uint32_t sv[2];
+          sv[0] = rna_tf32(sx);
+          sv[1] = rna_tf32(sx - __uint_as_float(sv[0]));
+          // place the window in the scratch row (clearing the previous window), read the dense
+          // row back, and store it with warp-uniform TMEM column addresses
+#pragma unroll
+          for (int t = 0; t < 4; t++) {
+            scr[base_old + t] = 0u;
+            scr[FPP + base_old + t] = 0u;
+          }
+#pragma unroll
+          for (int t = 0; t < 4; t++) {
+            scr[base + t] = wh[t];
+            scr[FPP + base + t] = wl[t];
+          }
+          scr[a.R] = sv[0];
+          scr[FPP + a.R] = sv[1];
+          uint32_t hi[FPP], lo[FPP];
+#pragma unroll
+          for (int w = 0; w < FPP; w += 4) {
+            const uint4 h = *reinterpret_cast<const uint4*>(scr + w);
+            const uint4 l = *reinterpret_cast<const uint4*>(scr + FPP + w);
+            hi[w] = h.x, hi[w + 1] = h.y, hi[w + 2] = h.z, hi[w + 3] = h.w;
+            lo[w] = l.x, lo[w + 1] = l.y, lo[w + 2] = l.z, lo[w + 3] = l.w;
+          }
+          constexpr int SW = FP % 8 == 0 ? 8 : (FP % 4 == 0 ? 4 : 2);  // tcgen05.st width
+          const uint32_t at = tmem + lane_base + A0 + ab * 2 * KC + fs * FP;
+#pragma unroll
+          for (int w = 0; w < FP / SW; w++) {
+            tm_stw<SW>(at + SW * w, hi + SW * w);
+            tm_stw<SW>(at + KC + SW * w, lo + SW * w);
+          }
+          tm_wait_st();
+          bq[NA - 1] = base;
+        } else {
+          bq[NA - 1] = base_old;
+        }
+        tm_fence_before();
+        mbar_arrive(&a_full[ab]);
+        if (c > 0) drain(q - 1);  // the previous chunk, now that this one is queued
+      }
+      if (nch > 0) drain(q - 1);  // the item's last chunk
+      if (vrow) {
+        float* yr = a.Y + row * a.m + nt * N + fs * CPS;
+        if (nt * N + (fs + 1) * CPS <= a.m && (a.m & 3) == 0) {
+#pragma unroll
+          for (int n = 0; n < CPS; n += 4)
+            *reinterpret_cast<float4*>(yr + n) =
+                make_float4((float)acc[n], (float)acc[n + 1], (float)acc[n + 2], (float)acc[n + 3]);
+        } else {
+#pragma unroll
+          for (int n = 0; n < CPS; n++)
+            if (nt * N + fs * CPS + n < a.m) yr[n] = (float)acc[n];
+        }
+      }
+    }
+  }
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kAlloc) : "memory");
+}
+
+// Bm in UMMA blocks: block (nt, c) holds hi then lo, element (n, k) of each at
+// (n % 8) * 16 + (n / 8) * (KC / 4) * 128 + (k % 4) * 4 + (k / 4) * 128 bytes; k = ii * FP + f.
+__global__ void build_spline_tc_kernel(const double* coeffs, const double* gains, float* B, int32_t d, int32_t m,
+                                       int32_t R, int32_t N, int32_t FP, int32_t IC, int32_t n_ch, int64_t total) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= total) return;
+  const int KC = IC * FP;
+  const int64_t per_block = (int64_t)N * KC;
+  const int64_t blk = t / per_block;
+  const int rem = (int)(t - blk * per_block);
+  const int n = rem / KC, k = rem - n * KC;
+  const int nt = (int)(blk / n_ch), c = (int)(blk - (int64_t)nt * n_ch);
+  const int ii = k / FP, f = k - ii * FP;
+  const int i = c * IC + ii, j = nt * N + n;
+  double v = 0.0;
+  if (i < d && j < m) {
+    const int64_t E = (int64_t)d * m, e = (int64_t)i * m + j;
+    const double bs = gains[e], ss = gains[E + e], os = gains[2 * E + e];
+    if (f < R)
+      v = os * ss * coeffs[e * R + f];
+    else if (f == R)
+      v = os * bs;
+  }
+  const float vf = (float)v;
+  const uint32_t hb = (__float_as_uint(vf) + 0x1000u) & 0xFFFFE000u;
+  const float lof = vf - __uint_as_float(hb);
+  const uint32_t lb = (__float_as_uint(lof) + 0x1000u) & 0xFFFFE000u;
+  const int64_t off = (int64_t)(n % 8) * 4 + (int64_t)(n / 8) * (KC / 4) * 32 + (k % 4) + (int64_t)(k / 4) * 32;
+  float* base = B + blk * 2 * per_block;
+  base[off] = __uint_as_float(hb);
+  base[per_block + off] = __uint_as_float(lb);
+}
+
+}  // namespace
+
+namespace lkg {
+
+static int tc_fp(int R) {  // features per input: R basis + silu, rounded up to an even count (<= 16)
+  const int f = R + 1;   // or to 20 (two inputs per 40-column chunk)
+  return f <= 16 ? (f + 1) / 2 * 2 : 20;
+}
+
+// The tensor-core spline applies to uniform cubic grids with R + 1 <= 20 features per input.
+bool spline_tc_eligible(const lkg_spec* S) {
+  if (S->degree != 3 || S->K < 1 || tc_fp(S->K + 3) > 20) return false;
+  double hmin = 1e300, hmax = 0;
+  for (int k = 0; k < S->K; k++) {
+    hmin = std::min(hmin, S->breakpoints[k + 1] - S->breakpoints[k]);
+    hmax = std::max(hmax, S->breakpoints[k + 1] - S->breakpoints[k]);
+  }
+  return hmax <= hmin * (1.0 + 1e-9);
+}
+
+static int tc_n(int m) { return m <= 16 ? 16 : (m <= 32 ? 32 : 64); }
+
+static void build_spline_tc(lkg_ctx* ctx, lkg_spec* S) {
+  if (S->tc_b.p) return;
+  const int d = S->in_dim, m = S->col1 - S->col0, R = S->K + 3, FP = tc_fp(R), IC = FP <= 16 ? 4 : 2;
+  const int N = tc_n(m), n_nt = (m + N - 1) / N, n_ch = (d + IC - 1) / IC;
+  const int64_t total = (int64_t)n_nt * n_ch * N * IC * FP;
+  S->tc_b.alloc(sizeof(float) * 2 * total);
+  S->tc_n_ch = n_ch;
+  build_spline_tc_kernel<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(
+      S->coeffs.as<double>(), S->gains.as<double>(), S->tc_b.as<float>(), d, m, R, N, FP, IC, n_ch, total);
+  LKG_CUDA(cudaGetLastError());
+  ctx->launches++;
+}
+
+template <int N, int FP>
+static void launch_tc_t(lkg_ctx* ctx, const TcArgs& a, int grid) {
+  constexpr int IC = FP <= 16 ? 4 : 2, KC = IC * FP;
+  constexpr int FPP = (FP + 3) / 4 * 4, SCR = 2 * FPP + 4;
+  const size_t smem = (size_t)NSB * 2 * N * KC * 4 + 1024 + (size_t)32 * (4 * NFS + 2) * SCR * 4;
+  static bool attr = false;
+  if (!attr) {
+    LKG_CUDA(cudaFuncSetAttribute(spline_tc<N, FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  spline_tc<N, FP><<<grid, 32 * (4 * NFS + 2), smem, ctx->stream>>>(a);
+}
+
+bool launch_spline_tc(lkg_ctx* ctx, const lkg_spec* S_, const float* X, int64_t rows, float* Y) {
+  lkg_spec* S = const_cast<lkg_spec*>(S_);
+  if (!spline_tc_eligible(S)) return false;
+  build_spline_tc(ctx, S);
+  const int d = S->in_dim, m = S->col1 - S->col0, R = S->K + 3, FP = tc_fp(R), IC = FP <= 16 ? 4 : 2;
+  const int N = tc_n(m);
+  TcArgs a{};
+  a.X = X;
+  a.rows = rows;
+  a.d = d;
+  a.Y = Y;
+  a.m = m;
+  a.B = S->tc_b.as<uint8_t>();
+  a.n_nt = (m + N - 1) / N;
+  a.n_ch = S->tc_n_ch;
+  a.IC = IC;
+  a.R = R;
+  a.n0 = S->K + 6;  // intervals of the extended knot vector (K + 2p)
+  // The tensor cores add each MMA's result into the fp32 accumulator with a one-sided rounding
+  // (measured: ~0.5 ulp of |D| per MMA, biased), so D holds ONE chunk (3 x KC/8 MMAs) and the
+  // feature warps add it into round-to-nearest fp32 registers after every chunk
+  // (tools/spline_tc_recipes.py: within the 1e-5 bar on C1-C4; 64-input groups reached 6x the bar).
+  a.gch = 1;
+  static const char* dbg = getenv("LKG_TC_DBG");
+  a.dbg = dbg ? atoi(dbg) : 0;
+  const double h = (S->breakpoints[S->K] - S->breakpoints[0]) / S->K;
+  a.t0 = (float)(S->breakpoints[0] - 3.0 * (S->breakpoints[1] - S->breakpoints[0]));
+  a.inv_h = (float)(1.0 / h);
+  a.n_rt = (rows + TM - 1) / TM;
+  a.n_items = a.n_rt * a.n_nt;
+  // instruction descriptor: D f32, A/B tf32, K-major both, N >> 3, M = 128 >> 4
+  a.idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  const int grid = (int)std::min<int64_t>(a.n_items, sms);
+#define LKG_TC(NN, FF)                                  \
+  if (N == NN && FP == FF) {                            \
+    launch_tc_t<NN, FF>(ctx, a, grid);                  \
+    LKG_CUDA(cudaGetLastError());                       \
+    ctx->launches++;                                    \
+    return true;                                        \
+  }
+  LKG_TC(16, 6) LKG_TC(16, 8) LKG_TC(16, 10) LKG_TC(16, 12) LKG_TC(16, 14) LKG_TC(16, 16) LKG_TC(16, 20)
+  LKG_TC(32, 6) LKG_TC(32, 8) LKG_TC(32, 10) LKG_TC(32, 12) LKG_TC(32, 14) LKG_TC(32, 16) LKG_TC(32, 20)
+  LKG_TC(64, 6) LKG_TC(64, 8) LKG_TC(64, 10) LKG_TC(64, 12) LKG_TC(64, 14) LKG_TC(64, 16) LKG_TC(64, 20)
+#undef LKG_TC
+  return false;
+}
+
+}  // namespace lkg
