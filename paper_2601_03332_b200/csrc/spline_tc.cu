@@ -207,13 +207,16 @@ __global__ void __launch_bounds__(32 * (4 * NFS + 2), 1) spline_tc(const __grid_
           tm_fence_after();
           const uint32_t a_hi = tmem + A0 + ab * 2 * KC, a_lo = a_hi + KC, d_t = tmem + D0 + db * N;
           const uint32_t bhi = lkg::smem_u32(bst + s * kBlock), blo = bhi + N * KC * 4;
+          // the small cross terms first (while |D| is ~2^-11 of the chunk's sum their one-sided
+          // rounding is negligible), then the KC/8 hi*hi products: a third of the MMAs round at |D|
 #pragma unroll
-          for (int ks = 0; ks < KC / 8; ks++) {
-            if (a.dbg & 1) break;
-            umma_tf32(d_t, a_hi + 8 * ks, b_desc(bhi + ks * 256, sbo), a.idesc, ks == 0 ? 0u : 1u);
-            umma_tf32(d_t, a_hi + 8 * ks, b_desc(blo + ks * 256, sbo), a.idesc, 1u);
+          for (int ks = 0; ks < KC / 8 && !(a.dbg & 1); ks++) {
+            umma_tf32(d_t, a_hi + 8 * ks, b_desc(blo + ks * 256, sbo), a.idesc, ks == 0 ? 0u : 1u);
             umma_tf32(d_t, a_lo + 8 * ks, b_desc(bhi + ks * 256, sbo), a.idesc, 1u);
           }
+#pragma unroll
+          for (int ks = 0; ks < KC / 8 && !(a.dbg & 1); ks++)
+            umma_tf32(d_t, a_hi + 8 * ks, b_desc(bhi + ks * 256, sbo), a.idesc, 1u);
           umma_commit(&b_empty[s]);
           umma_commit(&a_empty[ab]);
           umma_commit(&d_full[db]);

@@ -14,10 +14,14 @@ from oracle.pyoracle import Oracle  # noqa: E402
 
 o = Oracle("auto")
 for cfg, layer, rows in ((1, 0, 4096), (1, 1, 4096), (2, 0, 20000), (2, 1, 20000), (3, 0, 4000), (3, 1, 4000),
-                         (4, 0, 256), (4, 1, 256), (4, 2, 1024), (5, 0, 32)):
+                         (4, 0, 256), (4, 1, 256), (4, 2, 1024), (4, 2, -256), (5, 0, 32)):
     spec = lk.recipe_layer(cfg, layer) if cfg != 5 else lk.recipe_layer(5, 0, 0, 256)
+    wide = rows < 0      # tests/test_gpu_parity.py::test_spline_forward's hidden inputs U(-2.5, 2.5)
+    rows = abs(rows)
     if layer == 0:
         X = lk.recipe_inputs(cfg, 0, rows)
+    elif wide:
+        X = np.random.default_rng(1000 * cfg + layer).uniform(-2.5, 2.5, (rows, spec.in_dim)).astype(np.float32)
     else:
         X = np.random.default_rng(cfg).uniform(-1.3, 1.3, (rows, spec.in_dim)).astype(np.float32)
     Y = lk.layer_forward_batch(spec, torch.from_numpy(X).cuda()).cpu().numpy().astype(np.float64)
