@@ -417,7 +417,7 @@ static int tc_fp(int R) {  // features per input: R basis + silu, rounded up to 
 
 // The tensor-core spline applies to uniform cubic grids with R + 1 <= 20 features per input.
 bool spline_tc_eligible(const lkg_spec* S) {
-  if (S->degree != 3 || S->K < 1 || tc_fp(S->K + 3) > 20) return false;
+  if (S->degree != 3 || S->K < 1 || S->K + 3 + 1 > 20) return false;  // R basis + silu <= 20 features
   double hmin = 1e300, hmax = 0;
   for (int k = 0; k < S->K; k++) {
     hmin = std::min(hmin, S->breakpoints[k + 1] - S->breakpoints[k]);
