@@ -518,18 +518,28 @@ def main():
             for l in range(nl):
                 lk.lutkan.check(lib().lkg_spline_forward(eng.handle, sdev[l].handle, C.c_void_p(bufs[l].data_ptr()),
                                                          rows, C.c_void_p(bufs[l + 1].data_ptr())))
-        spline_step()
-        barrier()
-        ks = max(3, min(args.steps, 20))
-        e0.record(stream)
-        for _ in range(ks):
+        def time_spline():
             spline_step()
-        e1.record(stream)
-        barrier()
-        ms_s = e0.elapsed_time(e1) / ks
+            barrier()
+            ks = max(3, min(args.steps, 20))
+            e0.record(stream)
+            for _ in range(ks):
+                spline_step()
+            e1.record(stream)
+            barrier()
+            return e0.elapsed_time(e1) / ks
+        ms_s = time_spline()                      # tensor-core GEMM form (spline_tc.cu) where eligible
         spline_out = bufs[nl].cpu().numpy()
+        eng.set_spline_kernel("simt")
+        ms_simt = time_spline()                   # the SIMT table kernel (spline_tiled.cu)
+        eng.set_spline_kernel("auto")
         spline = {"value": rows * ee_row / (ms_s * 1e-3), "unit": "edge-evals/s", "ms_per_step": ms_s,
-                  "lut_speedup": ms_s / ms, "kernel": "spline_forward (Cox-de Boor, fp32 terms, f64 accumulation)"}
+                  "lut_speedup": ms_s / ms,
+                  "kernel": "spline_forward on the tensor cores (spline_tc.cu: basis x coefficient GEMM, "
+                            "tcgen05.mma kind::tf32 3xTF32, f64 chunk accumulation)",
+                  "simt": {"value": rows * ee_row / (ms_simt * 1e-3), "ms_per_step": ms_simt,
+                           "lut_speedup": ms_simt / ms,
+                           "kernel": "spline_tiled.cu (SIMT, fp32 terms, f64 accumulation for d > 256)"}}
 
     # end to end through the host-buffer entry point
     e2e = None

@@ -211,6 +211,12 @@ lkg_status lkg_ctx_collect(lkg_ctx* ctx, lkg_oob_stats* stats, int32_t n_layers)
 /* layer_forward_batch(spec, X, Tier::Optimized) (spline.cpp:145-187); device pointers. */
 lkg_status lkg_spline_forward(lkg_ctx* ctx, const lkg_spec* spec, const float* X, int64_t rows,
                               float* Y);
+/* Spline kernel family used by this context's lkg_spline_forward[_host]:
+ * LKG_SPLINE_AUTO (default): the tensor-core GEMM form (spline_tc.cu: uniform cubic grids with
+ *   K <= 16), else the SIMT table kernel (uniform cubic), else the generic Cox-de Boor kernel;
+ * LKG_SPLINE_SIMT: skip the tensor-core form (the SIMT kernels, for the same-GPU comparison). */
+enum { LKG_SPLINE_AUTO = 0, LKG_SPLINE_SIMT = 1 };
+lkg_status lkg_ctx_set_spline_kernel(lkg_ctx* ctx, int32_t kind);
 /* Same with HOST buffers (H2D of X, kernel, D2H of Y; synchronous). */
 lkg_status lkg_spline_forward_host(lkg_ctx* ctx, const lkg_spec* spec, const float* X_host, int64_t rows,
                                    float* Y_host);

@@ -238,6 +238,13 @@ lkg_status lkg_ctx_synchronize(lkg_ctx* ctx) {
 }
 
 void* lkg_ctx_stream(lkg_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+lkg_status lkg_ctx_set_spline_kernel(lkg_ctx* ctx, int32_t kind) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (kind != LKG_SPLINE_AUTO && kind != LKG_SPLINE_SIMT) fail(LKG_ERR_INVALID_ARG, "unknown spline kernel");
+    ctx->spline_kernel = kind;
+  });
+}
 uint64_t lkg_ctx_launch_count(lkg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 // ------------------------------------------------------------------- layers

@@ -133,6 +133,7 @@ struct lkg_ctx {
   cudaStream_t copy_stream = nullptr;  // H2D of the next chunk overlaps the chain on `stream`
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
   cudaStream_t comm_stream = nullptr;  // sharded chain: all-gathers overlap the next chunk's compute
+  int32_t spline_kernel = 0;  // LKG_SPLINE_AUTO / LKG_SPLINE_SIMT (lkg_ctx_set_spline_kernel)
   void* nccl = nullptr;  // ncclComm_t
   int32_t nranks = 1, rank = 0;
 };

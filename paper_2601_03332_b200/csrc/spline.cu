@@ -132,9 +132,11 @@ void launch_spline(lkg_ctx* ctx, const lkg_spec* S, const float* X, int64_t rows
                    const float* /*d_ext*/) {
   if (rows <= 0) return;
   static const bool force_simple = getenv("LKG_SPLINE_SIMPLE") != nullptr;  // test hook
-  // tensor-core GEMM form first (spline_tc.cu); LKG_SPLINE_SIMT=1 keeps the SIMT table kernel
+  // tensor-core GEMM form first (spline_tc.cu) unless the context asks for the SIMT kernels
+  // (lkg_ctx_set_spline_kernel) or LKG_SPLINE_SIMT=1 (experiment hook)
   static const char* simt = getenv("LKG_SPLINE_SIMT");
-  if (!force_simple && !(simt && simt[0] == '1') && launch_spline_tc(ctx, S, X, rows, Y)) return;
+  const bool no_tc = (simt && simt[0] == '1') || ctx->spline_kernel == LKG_SPLINE_SIMT;
+  if (!force_simple && !no_tc && launch_spline_tc(ctx, S, X, rows, Y)) return;
   if (!force_simple && launch_spline_tiled(ctx, S, X, rows, Y)) return;
   std::vector<double> ext;
   knot_grid(S->breakpoints, S->degree, ext);

@@ -255,6 +255,10 @@ class Engine:
         check(lib().lkg_ctx_collect(self.handle, arr, n_layers))
         return [OobStats._from(s) for s in arr]
 
+    def set_spline_kernel(self, kind: str) -> None:
+        """'auto' (tensor-core GEMM form where eligible) or 'simt' (the SIMT spline kernels)."""
+        check(lib().lkg_ctx_set_spline_kernel(self.handle, {"auto": 0, "simt": 1}[kind]))
+
     def init_nccl(self, uid: bytes, nranks: int, rank: int):
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         check(lib().lkg_ctx_init_nccl(self.handle, buf, nranks, rank))
