@@ -569,6 +569,20 @@ def main():
                "h2d_bytes_per_step": rows * dims[0] * 4, "d2h_bytes_per_step": rows * dims[-1] * 4,
                "ms_per_step": ms_e}
 
+    # end to end through the C++ drop-in shim with the reference's own f64 Matrix (the call a reference
+    # caller makes: lutkan_b200::lut_model_forward_batch), when the caller program was built here
+    e2e_shim = None
+    shim_bin = os.path.join(ROOT, "tools", "_bin", "shim_e2e")
+    if not args.no_e2e and args.workload == "c2" and os.path.exists(shim_bin) and world == 1:
+        try:
+            r = subprocess.run([shim_bin, str(rows), "5", "2"], capture_output=True, text=True, timeout=600)
+            e2e_shim = json.loads(r.stdout.strip().splitlines()[-1])
+            e2e_shim["api"] = ("lutkan_b200::lut_model_forward_batch(chain, lutkan::Matrix f64) -> "
+                               "lkg_model_forward_host_f64 (pageable f64 rows, narrowed/widened by host threads through pinned staging)")
+            e2e_shim["clock"] = "host wall clock per call, after 2 warm-up calls"
+        except Exception as ex:  # noqa: BLE001
+            e2e_shim = {"error": repr(ex)}
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "edge-evals/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -580,7 +594,7 @@ def main():
                            "accumulators in TMEM for d > 256")),
                 "data": "synthetic (BASELINE.json recipe, reference Rng; inputs > L2, no flush)",
                 "config": workload_config(args.workload, world),
-                "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roofline, "e2e": e2e, "e2e_shim_f64": e2e_shim, "gpu_launches": launches,
                 "oob_any_frac_layer0": stats[0].oob_any_frac(), "clocks": clk.summary(),
                 "spline_baseline": spline,
                 "compile": {"gpu_ms": compile_ms, "cold_ms": compile_cold_ms, "layers": nl,

@@ -184,6 +184,13 @@ lkg_status lkg_model_forward(lkg_ctx* ctx, const lkg_layer* const* chain, int32_
 lkg_status lkg_model_forward_host(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n_layers,
                                   const float* X_host, int64_t rows, float* Y_host,
                                   lkg_oob_stats* stats);
+/* Same call on the reference's own f64 rows (Matrix data, row-major, pageable): host threads narrow
+ * X to fp32 row chunk by row chunk into pinned staging while the previous chunk copies and runs; Y is
+ * widened back by the same threads. The C++ shim's lut_model_forward_batch / lut_layer_forward_batch
+ * go through this entry. */
+lkg_status lkg_model_forward_host_f64(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n_layers,
+                                      const double* X_host, int64_t rows, double* Y_host,
+                                      lkg_oob_stats* stats);
 /* A chain forward captured once as a CUDA graph and replayed: the same launches as
  * lkg_model_forward on the same DEVICE buffers (X, Y and the layers are bound at capture; rows > 0),
  * one cudaGraphLaunch per replay on ctx's stream, asynchronous. For small, latency-bound batches

@@ -219,15 +219,14 @@ inline lutkan::ChainBatchResult lut_model_forward_batch(const std::vector<lutkan
     throw lutkan::DimensionError("batch column count does not match artifact in_dim");
   std::vector<const lkg_layer*> dev;
   for (const auto& a : chain) dev.push_back(ctx.layer(a));
-  std::vector<float> x(X.data.begin(), X.data.end());  // documented: fp32 activations on device
   const size_t m = static_cast<size_t>(chain.back().out_dim);
-  std::vector<float> y(X.rows * m);
   std::vector<lkg_oob_stats> st(chain.size());
-  check(lkg_model_forward_host(ctx.get(), dev.data(), static_cast<int32_t>(dev.size()), x.data(),
-                               static_cast<int64_t>(X.rows), y.data(), st.data()));
   lutkan::ChainBatchResult r;
   r.Y = lutkan::Matrix(X.rows, m);
-  for (size_t i = 0; i < y.size(); i++) r.Y.data[i] = y[i];
+  // the f64 rows go to the device as they are and are narrowed there (documented: fp32 activations
+  // on the device), the fp32 outputs widened there
+  check(lkg_model_forward_host_f64(ctx.get(), dev.data(), static_cast<int32_t>(dev.size()), X.data.data(),
+                                   static_cast<int64_t>(X.rows), r.Y.data.data(), st.data()));
   for (const auto& s : st) r.per_layer.push_back(to_stats(s));
   return r;
 }
@@ -239,13 +238,11 @@ inline std::pair<lutkan::Matrix, lutkan::OobStats> lut_layer_forward_batch(
   if (X.cols != static_cast<size_t>(a.in_dim))
     throw lutkan::DimensionError("batch column count does not match artifact in_dim");
   const lkg_layer* dev = ctx.layer(a);
-  std::vector<float> x(X.data.begin(), X.data.end());
-  std::vector<float> y(X.rows * static_cast<size_t>(a.out_dim));
   lkg_oob_stats st{};
-  check(lkg_model_forward_host(ctx.get(), &dev, 1, x.data(), static_cast<int64_t>(X.rows), y.data(), &st));
   (void)tier;
   lutkan::Matrix Y(X.rows, static_cast<size_t>(a.out_dim));
-  for (size_t i = 0; i < y.size(); i++) Y.data[i] = y[i];
+  check(lkg_model_forward_host_f64(ctx.get(), &dev, 1, X.data.data(), static_cast<int64_t>(X.rows), Y.data.data(),
+                                   &st));
   return {std::move(Y), to_stats(st)};
 }
 

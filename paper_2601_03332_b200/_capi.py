@@ -93,6 +93,8 @@ SIGNATURES = {
     "lkg_ctx_collect": (C.c_int, [C.c_void_p, _P(OobStatsC), C.c_int32]),
     "lkg_spline_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "lkg_ctx_set_spline_kernel": (C.c_int, [C.c_void_p, C.c_int32]),
+    "lkg_model_forward_host_f64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
+                                             C.c_void_p]),
     "lkg_spline_forward_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "lkg_artifact_save": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p, C.c_int32]),
     "lkg_artifact_load": (C.c_int, [C.c_void_p, C.c_char_p, _P(C.c_void_p)]),

@@ -12,6 +12,8 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <atomic>
+#include <thread>
 #include <vector>
 
 #include "lkg_internal.h"
@@ -218,6 +220,7 @@ lkg_status lkg_ctx_destroy(lkg_ctx* ctx) {
       cudaStreamSynchronize(ctx->comm_stream);
       cudaStreamDestroy(ctx->comm_stream);
     }
+    if (ctx->pin) cudaFreeHost(ctx->pin);
     if (ctx->copy_stream) {
       cudaStreamSynchronize(ctx->copy_stream);
       cudaStreamDestroy(ctx->copy_stream);
@@ -786,6 +789,107 @@ lkg_status lkg_model_forward_host(lkg_ctx* ctx, const lkg_layer* const* chain, i
     if (rows > 0) LKG_CUDA(cudaMemcpyAsync(Yh, dY, yb, cudaMemcpyDeviceToHost, ctx->stream));
     if (stats) collect_impl(ctx, stats, n);
     else LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// The reference's own I/O type: f64 Matrix rows in and out (runtime.hpp:130-148), from pageable
+// host memory. Host threads narrow X to fp32 row chunk by row chunk into pinned staging (the
+// documented fp32 activations: static_cast<float>), each chunk's H2D (copy stream) and chain (context
+// stream) overlap the narrowing of the next; Y comes back through pinned staging and is widened by
+// the same threads. Chunk starts are multiples of kRowAlign rows (bit-identical to one launch).
+lkg_status lkg_model_forward_host_f64(lkg_ctx* ctx, const lkg_layer* const* chain, int32_t n, const double* Xh,
+                                      int64_t rows, double* Yh, lkg_oob_stats* stats) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    check_chain(chain, n);
+    if (rows < 0) fail(LKG_ERR_DIMENSION, "negative row count");
+    if (rows > 0) {
+      need(Xh, "X");
+      need(Yh, "Y");
+    }
+    DeviceGuard g(ctx->device);
+    const int64_t d = chain[0]->in_dim, mo = chain[n - 1]->out_dim;
+    const int64_t ch = (std::max<int64_t>(65536, (16ll << 20) / (4 * d)) + lkg::kRowAlign - 1) / lkg::kRowAlign *
+                       lkg::kRowAlign;
+    const int64_t nch = rows > ch ? (rows + ch - 1) / ch : 1, cr = nch > 1 ? ch : rows;
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    const size_t xb = up(sizeof(float) * cr * d), yb = up(sizeof(float) * rows * mo);
+    ensure(ctx->hostio, 2 * xb + yb + 256);
+    float* dX[2] = {ctx->hostio.as<float>(), reinterpret_cast<float*>(ctx->hostio.as<char>() + xb)};
+    float* dY = reinterpret_cast<float*>(ctx->hostio.as<char>() + 2 * xb);
+    if (ctx->pin_bytes < 2 * xb + yb) {
+      if (ctx->pin) LKG_CUDA(cudaFreeHost(ctx->pin));
+      ctx->pin = nullptr;
+      ctx->pin_bytes = 0;
+      LKG_CUDA(cudaMallocHost(&ctx->pin, 2 * xb + yb));
+      ctx->pin_bytes = 2 * xb + yb;
+    }
+    float* hX[2] = {static_cast<float*>(ctx->pin), reinterpret_cast<float*>(static_cast<char*>(ctx->pin) + xb)};
+    float* hY = reinterpret_cast<float*>(static_cast<char*>(ctx->pin) + 2 * xb);
+    if (!ctx->copy_stream) {
+      LKG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; b++) {
+        LKG_CUDA(cudaEventCreateWithFlags(&ctx->ev_copied[b], cudaEventDisableTiming));
+        LKG_CUDA(cudaEventCreateWithFlags(&ctx->ev_done[b], cudaEventDisableTiming));
+      }
+    }
+    const int T = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    // host workers: for chunk c, worker t narrows its slice into hX[c & 1] once the H2D of chunk c-2
+    // (the previous user of that staging buffer) has completed, then counts itself done
+    std::vector<std::atomic<int>> ready((size_t)std::max<int64_t>(nch, 1));
+    for (auto& r : ready) r.store(0);
+    std::atomic<int64_t> copied_upto{-1};  // chunks whose H2D was enqueued (event recorded)
+    std::atomic<bool> abort{false};
+    auto worker = [&](int t) {
+      for (int64_t c = 0; c < nch && rows > 0 && !abort.load(); c++) {
+        const int b = (int)(c & 1);
+        const int64_t r0 = c * ch, nr = std::min(cr, rows - r0), ne = nr * d;
+        if (c >= 2) {
+          while (copied_upto.load(std::memory_order_acquire) < c - 2 && !abort.load()) std::this_thread::yield();
+          if (cudaEventSynchronize(ctx->ev_copied[b]) != cudaSuccess) abort.store(true);
+        }
+        const int64_t e0 = ne * t / T, e1 = ne * (t + 1) / T;
+        const double* src = Xh + r0 * d;
+        float* dst = hX[b];
+        for (int64_t e = e0; e < e1; e++) dst[e] = static_cast<float>(src[e]);
+        ready[(size_t)c].fetch_add(1, std::memory_order_release);
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; t++) pool.emplace_back(worker, t);
+    try {
+      for (int64_t c = 0; c < nch && rows > 0; c++) {
+        const int b = (int)(c & 1);
+        const int64_t r0 = c * ch, nr = std::min(cr, rows - r0);
+        while (ready[(size_t)c].load(std::memory_order_acquire) < T) std::this_thread::yield();
+        if (c >= 2) LKG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_done[b], 0));
+        LKG_CUDA(cudaMemcpyAsync(dX[b], hX[b], sizeof(float) * nr * d, cudaMemcpyHostToDevice, ctx->copy_stream));
+        LKG_CUDA(cudaEventRecord(ctx->ev_copied[b], ctx->copy_stream));
+        copied_upto.store(c, std::memory_order_release);
+        LKG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_copied[b], 0));
+        run_chain(ctx, chain, n, dX[b], nr, dY + r0 * mo);
+        LKG_CUDA(cudaEventRecord(ctx->ev_done[b], ctx->stream));
+      }
+    } catch (...) {
+      abort.store(true);
+      copied_upto.store(nch);
+      for (auto& th : pool) th.join();
+      throw;
+    }
+    for (auto& th : pool) th.join();
+    if (abort.load()) fail(LKG_ERR_CUDA, "host staging of the f64 input failed");
+    if (rows > 0) LKG_CUDA(cudaMemcpyAsync(hY, dY, sizeof(float) * rows * mo, cudaMemcpyDeviceToHost, ctx->stream));
+    if (stats) collect_impl(ctx, stats, n);
+    else LKG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (rows > 0) {
+      const int64_t ny = rows * mo;
+      std::vector<std::thread> wid;
+      for (int t = 0; t < T; t++)
+        wid.emplace_back([&, t] {
+          for (int64_t e = ny * t / T; e < ny * (t + 1) / T; e++) Yh[e] = static_cast<double>(hY[e]);
+        });
+      for (auto& th : wid) th.join();
+    }
   });
 }
 
