@@ -4,4 +4,5 @@ ncu --set full --import-source on --clock-control none -k regex:${KREGEX:-fwd_ti
     python ${PROF:-tools/prof_forward.py} $wl $layer 2 > gpurun_out/ncu_$tag.log 2>&1
 python tools/ncu_summary.py gpurun_out/ncu_$tag.ncu-rep "$wl layer $layer ($tag)" > gpurun_out/ncu_$tag.txt 2>&1
 ncu -i gpurun_out/ncu_$tag.ncu-rep --page raw --csv > gpurun_out/ncu_${tag}_raw.csv 2>/dev/null
+[ -n "$SRC" ] && ncu -i gpurun_out/ncu_$tag.ncu-rep --page source --csv --print-source sass 2>/dev/null | gzip > gpurun_out/ncu_${tag}_sass.csv.gz
 [ -n "$KEEP_REP" ] || rm -f gpurun_out/ncu_$tag.ncu-rep
