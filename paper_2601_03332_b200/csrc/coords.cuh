@@ -93,10 +93,12 @@ __device__ __forceinline__ float silu_exact(float x) {
 __device__ __forceinline__ float floor_magic(float v) { return __fadd_rd(v, 8388608.0f); }
 __device__ __forceinline__ int floor_magic_int(float m) { return __float_as_int(m) - 0x4B000000; }
 
-__device__ __forceinline__ Coord lut_coords_fast_nb(const CoordConst& c, const float4* ktab, float x, bool& slow) {
+// kf: the compact per-segment table {T_k, (L-1)/h_k} (8-byte entries: a warp's 64-bit loads of up to
+// 16 distinct segments hit distinct banks; the 16-byte ktab rows conflicted for K > 8)
+__device__ __forceinline__ Coord lut_coords_fast_nb(const CoordConst& c, const float2* kf, float x, bool& slow) {
   const float xp = fminf(fmaxf(x, c.lo), c.hi_clip);
   const int k = min(floor_magic_int(floor_magic((xp - c.lo) * c.inv_h)), c.K - 1);
-  const float2 kt = *reinterpret_cast<const float2*>(ktab + k);  // {T_k, (L-1)/h_k}
+  const float2 kt = kf[k];  // {T_k, (L-1)/h_k}
   const float dx = xp - kt.x, z1 = fmaf(dx, kt.y, 1.0f), zm = floor_magic(z1), zf = zm - 8388608.0f;
   const float w1 = z1 - zf;
   const bool top = xp == c.hi_clip;
@@ -110,10 +112,10 @@ __device__ __forceinline__ Coord lut_coords_fast_nb(const CoordConst& c, const f
   return o;
 }
 
-__device__ __forceinline__ Coord lut_coords_fast(const CoordConst& c, const float4* ktab, float x) {
+__device__ __forceinline__ Coord lut_coords_fast(const CoordConst& c, const float4* ktab, const float2* kf, float x) {
   const float xp = fminf(fmaxf(x, c.lo), c.hi_clip);
   const int k = min(floor_magic_int(floor_magic((xp - c.lo) * c.inv_h)), c.K - 1);
-  const float2 kt = *reinterpret_cast<const float2*>(ktab + k);  // {T_k, (L-1)/h_k}
+  const float2 kt = kf[k];  // {T_k, (L-1)/h_k}
   const float dx = xp - kt.x, z1 = fmaf(dx, kt.y, 1.0f), zm = floor_magic(z1), zf = zm - 8388608.0f;
   const float w1 = z1 - zf;
   const bool top = xp == c.hi_clip;  // exact host-side coordinates; dx == 0: z = 0 exactly

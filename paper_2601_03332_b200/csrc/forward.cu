@@ -95,11 +95,15 @@ struct CoordArgs {
 __global__ void coords_tiled_kernel(const __grid_constant__ CoordArgs c, const float* x, int64_t n,
                                     int32_t* in_range, int32_t* k, int32_t* l0) {
   __shared__ float4 ktab[lkg::kMaxKT];
-  for (int q = threadIdx.x; q < c.cc.K; q += blockDim.x) ktab[q] = c.ktab[q];
+  __shared__ float2 kf[lkg::kMaxKT];
+  for (int q = threadIdx.x; q < c.cc.K; q += blockDim.x) {
+    ktab[q] = c.ktab[q];
+    kf[q] = make_float2(c.ktab[q].x, c.ktab[q].y);
+  }
   __syncthreads();
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  const lkg::Coord co = lkg::lut_coords_fast(c.cc, ktab, x[t]);  // the table walk's own path
+  const lkg::Coord co = lkg::lut_coords_fast(c.cc, ktab, kf, x[t]);  // the table walk's own path
   if (in_range) in_range[t] = co.in;
   if (k) k[t] = co.k;
   if (l0) l0[t] = co.l0;

@@ -198,12 +198,20 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   uint64_t* full = reinterpret_cast<uint64_t*>(ktab + kMaxKT);
   uint32_t* fin = reinterpret_cast<uint32_t*>(full + 4);  // warps done with each stage buffer
   uint64_t* xbar = full + 8;  // XT: per-warp x-block barriers (W <= 16)
-  float4* ktab2 = reinterpret_cast<float4*>(full + 24);
+  float2* kf = reinterpret_cast<float2*>(full + 24);  // compact {T_k, (L-1)/h_k} (coords.cuh)
+  float2* kf2 = kf + kMaxKT;
+  float4* ktab2 = reinterpret_cast<float4*>(kf2 + kMaxKT);
   uint8_t* lut2 = reinterpret_cast<uint8_t*>(ktab2 + kMaxKT);
 
-  for (int k = tid; k < a.cc.K; k += W * 32) ktab[k] = a.ktab[k];
+  for (int k = tid; k < a.cc.K; k += W * 32) {
+    ktab[k] = a.ktab[k];
+    kf[k] = make_float2(a.ktab[k].x, a.ktab[k].y);
+  }
   if (FUSE) {
-    for (int k = tid; k < a.cc2.K; k += W * 32) ktab2[k] = a.ktab2[k];
+    for (int k = tid; k < a.cc2.K; k += W * 32) {
+      ktab2[k] = a.ktab2[k];
+      kf2[k] = make_float2(a.ktab2[k].x, a.ktab2[k].y);
+    }
     for (int o = tid * 16; o < a.lut2_bytes; o += W * 32 * 16)
       *reinterpret_cast<uint4*>(lut2 + o) = __ldg(reinterpret_cast<const uint4*>(a.lut2 + o));
   }
@@ -401,7 +409,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
 #pragma unroll
           for (int r = 0; r < R; r++) {
             xv[r] = xs[il * XS + lane + 32 * r];
-            cv[r] = lkg::lut_coords_fast_nb(a.cc, ktab, xv[r], slow_r[r]);
+            cv[r] = lkg::lut_coords_fast_nb(a.cc, kf, xv[r], slow_r[r]);
             any_slow |= slow_r[r];
           }
           if (any_slow) {
@@ -411,7 +419,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           }
         } else {
           xv[0] = xs[il * XS + lane];
-          cv[0] = lkg::lut_coords_fast(a.cc, ktab, xv[0]);
+          cv[0] = lkg::lut_coords_fast(a.cc, ktab, kf, xv[0]);
           (void)any_slow;
           (void)slow_r;
         }
@@ -621,8 +629,8 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
             if (i2 < a.m) {
               const float h0 = out[i2], h1 = i2 + 1 < a.m ? out[i2 + 1] : a.cc2.lo;
               bool s0, s1;
-              lkg::Coord c0 = lkg::lut_coords_fast_nb(a.cc2, ktab2, h0, s0);
-              lkg::Coord c1 = lkg::lut_coords_fast_nb(a.cc2, ktab2, h1, s1);
+              lkg::Coord c0 = lkg::lut_coords_fast_nb(a.cc2, kf2, h0, s0);
+              lkg::Coord c1 = lkg::lut_coords_fast_nb(a.cc2, kf2, h1, s1);
               if (s0 || s1) {
                 if (s0) c0 = lkg::lut_coords(a.cc2, ktab2, h0);
                 if (s1) c1 = lkg::lut_coords(a.cc2, ktab2, h1);
@@ -755,10 +763,14 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* lut = smem;
   float4* ktab = reinterpret_cast<float4*>(smem + ((a.lut_bytes + 15) & ~15));
+  float2* kf = reinterpret_cast<float2*>(ktab + kMaxKT);  // compact {T_k, (L-1)/h_k} (coords.cuh)
   const int tid = threadIdx.x, lane = tid & 31;
   for (int o = tid * 16; o < a.lut_bytes; o += blockDim.x * 16)
     *reinterpret_cast<uint4*>(lut + o) = __ldg(reinterpret_cast<const uint4*>(a.lut + o));
-  for (int k = tid; k < a.cc.K; k += blockDim.x) ktab[k] = a.ktab[k];
+  for (int k = tid; k < a.cc.K; k += blockDim.x) {
+    ktab[k] = a.ktab[k];
+    kf[k] = make_float2(a.ktab[k].x, a.ktab[k].y);
+  }
   __syncthreads();
   const float lo = a.cc.lo;
   const int K = a.cc.K, L = a.cc.L, d = a.d, MP = VT ? MPT : a.MP;
@@ -860,8 +872,8 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
         const int inx = (i + 2 == d) ? 0 : i + 2;
         if (vrow && t + 2 < d) xn = __ldg(reinterpret_cast<const float2*>(x_ptr(inx)));
         bool s0, s1;
-        lkg::Coord c0 = lkg::lut_coords_fast_nb(a.cc, ktab, xx.x, s0);
-        lkg::Coord c1 = lkg::lut_coords_fast_nb(a.cc, ktab, xx.y, s1);
+        lkg::Coord c0 = lkg::lut_coords_fast_nb(a.cc, kf, xx.x, s0);
+        lkg::Coord c1 = lkg::lut_coords_fast_nb(a.cc, kf, xx.y, s1);
         if (s0 || s1) {
           if (s0) c0 = lkg::lut_coords(a.cc, ktab, xx.x);
           if (s1) c1 = lkg::lut_coords(a.cc, ktab, xx.y);
@@ -891,8 +903,8 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
         }
         const bool two = t + 1 < d;
         bool s0, s1;
-        lkg::Coord c0 = lkg::lut_coords_fast_nb(a.cc, ktab, xa, s0);
-        lkg::Coord c1 = lkg::lut_coords_fast_nb(a.cc, ktab, two ? xb : lo, s1);
+        lkg::Coord c0 = lkg::lut_coords_fast_nb(a.cc, kf, xa, s0);
+        lkg::Coord c1 = lkg::lut_coords_fast_nb(a.cc, kf, two ? xb : lo, s1);
         if (s0 || s1) {
           if (s0) c0 = lkg::lut_coords(a.cc, ktab, xa);
           if (s1) c1 = lkg::lut_coords(a.cc, ktab, xb);
@@ -911,7 +923,7 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
       for (int t = 0; t < d; t++, i = (i + 1 == d) ? 0 : i + 1) {
         const float x = xn;
         if (vrow && t + 1 < d) xn = __ldg(x_ptr(i + 1 == d ? 0 : i + 1));
-        const lkg::Coord co = lkg::lut_coords_fast(a.cc, ktab, x);
+        const lkg::Coord co = lkg::lut_coords_fast(a.cc, ktab, kf, x);
         nfacc = fmaf(x, 0.0f, nfacc);
         accum(i, x, co);
       }
@@ -1202,12 +1214,12 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   // Pair lines (twice the code bytes, no PRMT) only on request (LKG_IDP=1) and where two stage
   // buffers of them fit: measured on configs[1] layer 0 they lose to the standard lines (0.496 vs
   // 0.446 ms), which leave room for the second x buffer and halve the TMA bytes per tile.
-  if (idp && idp_env && idp_env[0] == '1' && !force_gc && 2 * layout(1) + xs_bytes + kMaxKT * 16 + 64 <= 227 * 1024)
+  if (idp && idp_env && idp_env[0] == '1' && !force_gc && 2 * layout(1) + xs_bytes + kMaxKT * 32 + 256 <= 227 * 1024)
     idp = 1;
   int64_t off = layout(idp == 1 ? 1 : 0);
   gm.idp = idp;
-  gm.codes_global = force_gc || 2 * off + xs_bytes + kMaxKT * 16 + 64 > 227 * 1024;  // codes stay in global (L2)
-  if (gm.codes_global && 2 * (off - gm.p_off) + xs_bytes + kMaxKT * 16 + 64 > 227 * 1024) return;  // generic
+  gm.codes_global = force_gc || 2 * off + xs_bytes + kMaxKT * 32 + 256 > 227 * 1024;  // codes stay in global (L2)
+  if (gm.codes_global && 2 * (off - gm.p_off) + xs_bytes + kMaxKT * 32 + 256 > 227 * 1024) return;  // generic
   gm.tile_bytes = off;
   gm.JB = JB;
   gm.IC = G;
@@ -1345,7 +1357,7 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
   fill_coord_const(L, a.cc, a.ktab);
   // one resident block per SM (1024 threads x ~47 registers) and one equal row range per block
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 1023) / 1024, sm_count(ctx->device)));
-  const size_t smem = ((gm.tile_bytes + 15) & ~15) + kMaxKT * 16;
+  const size_t smem = ((gm.tile_bytes + 15) & ~15) + kMaxKT * 16 + kMaxKT * 8;
   const bool asym = L->scheme == LKG_SCHEME_ASYMMETRIC, sr = L->value_repr == LKG_REPR_SPLINE_COMPONENT;
   const bool zs = L->oob_policy == LKG_OOB_ZERO_SPLINE;
   const int sz = (sr << 1) | (int)zs;
@@ -1377,7 +1389,8 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
 
 static size_t tiled_smem(const lkg_layer* L, int W, int R, int ns = LKG_NS, int xb = 1) {
   const int64_t sb = L->geom.tile_bytes - (L->geom.codes_global ? L->geom.p_off : 0);
-  return ns * sb + (size_t)xb * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 64 + 8 * 16;
+  // stages, x buffers, ktab, the barrier block (full/fin/xbar: 24 x 8 B), the compact tables kf, kf2
+  return ns * sb + (size_t)xb * W * G * (32 * R + 4) * 4 + kMaxKT * 16 + 24 * 8 + 2 * kMaxKT * 8;
 }
 
 

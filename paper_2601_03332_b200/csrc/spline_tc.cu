@@ -144,10 +144,11 @@ __global__ void __launch_bounds__(32 * (4 * NFS + 2), 1) spline_tc(const __grid_
   uint64_t *b_full = bar, *b_empty = bar + NSB, *a_full = bar + 2 * NSB, *a_empty = a_full + NA,
            *d_full = a_empty + NA, *d_empty = d_full + 2;
   uint32_t* tm_slot = reinterpret_cast<uint32_t*>(d_empty + 2);
-  // per-thread placement scratch: the input's FP features (hi row, then lo row), 2*FPP+4 words per
-  // thread (an odd number of 16-B units: the dense LDS.128 read-back is conflict-free)
-  constexpr int FPP = (FP + 3) / 4 * 4, SCR = 2 * FPP + 4;
-  uint32_t* scr = reinterpret_cast<uint32_t*>(smem + NSB * kBlock + 1024) + threadIdx.x * SCR;
+  // per-thread placement scratch: the input's FP features (hi, then lo), stored column-major across
+  // the CTA's threads (word (col, tid) at col * blockDim + tid): every STS / LDS of a warp hits 32
+  // distinct banks whatever column each thread addresses
+  constexpr int NT = 32 * (4 * NFS + 2);
+  uint32_t* scr = reinterpret_cast<uint32_t*>(smem + NSB * kBlock + 1024) + threadIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < NSB; s++) {
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(32 * (4 * NFS + 2), 1) spline_tc(const __grid_
     int bq[NA];  // window column of this thread's input in each A buffer's last use
 #pragma unroll
     for (int p = 0; p < NA; p++) bq[p] = 0;
-    for (int w = 0; w < SCR; w++) scr[w] = 0u;  // the placement scratch starts zeroed
+    for (int w = 0; w < 2 * FP; w++) scr[w * NT] = 0u;  // the placement scratch starts zeroed
     auto drain = [&](uint32_t qq) {  // chunk qq's D into acc
       const uint32_t db = qq & 1u;
       lkg::mbar_wait(&d_full[db], (qq >> 1) & 1u);
@@ -316,23 +317,21 @@ __global__ void __launch_bounds__(32 * (4 * NFS + 2), 1) spline_tc(const __grid_
           // row back, and store it with warp-uniform TMEM column addresses
 #pragma unroll
           for (int t = 0; t < 4; t++) {
-            scr[base_old + t] = 0u;
-            scr[FPP + base_old + t] = 0u;
+            scr[(base_old + t) * NT] = 0u;
+            scr[(FP + base_old + t) * NT] = 0u;
           }
 #pragma unroll
           for (int t = 0; t < 4; t++) {
-            scr[base + t] = wh[t];
-            scr[FPP + base + t] = wl[t];
+            scr[(base + t) * NT] = wh[t];
+            scr[(FP + base + t) * NT] = wl[t];
           }
-          scr[a.R] = sv[0];
-          scr[FPP + a.R] = sv[1];
-          uint32_t hi[FPP], lo[FPP];
+          scr[a.R * NT] = sv[0];
+          scr[(FP + a.R) * NT] = sv[1];
+          uint32_t hi[FP], lo[FP];
 #pragma unroll
-          for (int w = 0; w < FPP; w += 4) {
-            const uint4 h = *reinterpret_cast<const uint4*>(scr + w);
-            const uint4 l = *reinterpret_cast<const uint4*>(scr + FPP + w);
-            hi[w] = h.x, hi[w + 1] = h.y, hi[w + 2] = h.z, hi[w + 3] = h.w;
-            lo[w] = l.x, lo[w + 1] = l.y, lo[w + 2] = l.z, lo[w + 3] = l.w;
+          for (int w = 0; w < FP; w++) {
+            hi[w] = scr[w * NT];
+            lo[w] = scr[(FP + w) * NT];
           }
           constexpr int SW = FP % 8 == 0 ? 8 : (FP % 4 == 0 ? 4 : 2);  // tcgen05.st width
           const uint32_t at = tmem + lane_base + A0 + ab * 2 * KC + fs * FP;
@@ -444,8 +443,7 @@ static void build_spline_tc(lkg_ctx* ctx, lkg_spec* S) {
 template <int N, int FP>
 static void launch_tc_t(lkg_ctx* ctx, const TcArgs& a, int grid) {
   constexpr int IC = FP <= 16 ? 4 : 2, KC = IC * FP;
-  constexpr int FPP = (FP + 3) / 4 * 4, SCR = 2 * FPP + 4;
-  const size_t smem = (size_t)NSB * 2 * N * KC * 4 + 1024 + (size_t)32 * (4 * NFS + 2) * SCR * 4;
+  const size_t smem = (size_t)NSB * 2 * N * KC * 4 + 1024 + (size_t)32 * (4 * NFS + 2) * 2 * FP * 4;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(spline_tc<N, FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
