@@ -101,6 +101,7 @@ struct TiledArgs {
   lkg::CoordConst cc;        // coordinate constants (coords.cuh)
   int64_t n_items, n_rt;
   uint32_t rt_group;    // row tiles per item group (item_coords)
+  int32_t lgL;          // REC: log2(L)
   float4 ktab[kMaxKT];  // {T_k, (L-1)/(T_k+1 - T_k), T_k+1, 0}
   // fused next layer (FUSE): a small-out_dim layer evaluated in the epilogue from the 16 hidden
   // activations each lane holds (the whole-layer "small" layout, resident in shared memory)
@@ -169,7 +170,7 @@ __device__ __forceinline__ void item_coords(const TiledArgs& a, bool gc, uint32_
 }
 
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1, bool GC = false,
-          bool BAL = false, int XB = 1, bool XT = false, int IDPM = 0>
+          bool BAL = false, int XB = 1, bool XT = false, int IDPM = 0, bool REC = false>
 __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   // Two stage buffers, a compile-time count: NS as a runtime value turned every per-tile
@@ -402,10 +403,16 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
         const uint8_t* Tp = T + a.p_off + il * PROW;
         // ---- steps 1-4 (runtime.cpp:170-190): mask, clip, segment, coordinates (coords.cuh),
         // the R rows' fast chains side by side, then the exact path once for any that need it
+        // (REC: the coordinate pass did all of it once per input element; the box holds records)
         float xv[R];
         lkg::Coord cv[R];
         bool any_slow = false, slow_r[R];
-        if constexpr (R > 1) {  // measured: -2% time at R=2, +2% at R=1 (where it has nothing to pair)
+        if constexpr (REC) {
+          (void)any_slow;
+          (void)slow_r;
+#pragma unroll
+          for (int r = 0; r < R; r++) xv[r] = xs[il * XS + lane + 32 * r];
+        } else if constexpr (R > 1) {  // measured: -2% time at R=2, +2% at R=1 (where it has nothing to pair)
 #pragma unroll
           for (int r = 0; r < R; r++) {
             xv[r] = xs[il * XS + lane + 32 * r];
@@ -426,11 +433,29 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
 #pragma unroll
         for (int r = 0; r < R; r++) {
           const float x = xv[r];
-          const lkg::Coord co = cv[r];
-          const bool in = co.in;
-          const int k = co.k, l0 = co.l0;
-          const float xp = co.xp, w1 = co.w1;  // w1: multiple of 2^-23 -> exact magic constants
-          nfacc = fmaf(x, 0.0f, nfacc);  // NaN once any input is NaN or inf
+          bool in;
+          int k, l0;
+          float xp, w1;
+          uint32_t Wrec = 0;
+          if constexpr (REC) {
+            // record (coord_pass_kernel): W1 bits 0-14, code line k*L + l0 bits 15-27, OOB bit 31
+            const uint32_t rec = __float_as_uint(x);
+            in = (rec >> 31) == 0u;
+            const int line = (int)((rec >> 15) & 0x1FFFu);
+            k = line >> a.lgL;
+            l0 = line & (L - 1);
+            Wrec = (rec & 0x7FFFu) * 65535u + 32768u;
+            xp = 0.0f;
+            w1 = 0.0f;
+          } else {
+            const lkg::Coord co = cv[r];
+            in = co.in;
+            k = co.k;
+            l0 = co.l0;
+            xp = co.xp;
+            w1 = co.w1;  // w1: multiple of 2^-23 -> exact magic constants
+            nfacc = fmaf(x, 0.0f, nfacc);  // NaN once any input is NaN or inf
+          }
           if (!in) {  // (predicated adds: cheaper than materialising the flag)
             oob_item++;
             row_oob |= 1u << r;
@@ -449,7 +474,8 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
             // Integer lerp: W1 = round(w1 * 2^15), W0 = 2^15 - W1; one dp2a per output
             // gives 2^23 + W0*u0 + W1*u1 exactly as a magic float, one FADD2 per output pair removes
             // the magic (and the symmetric codes' +128 bias), P arrives pre-scaled by 2^-15.
-            const uint32_t Wd = __float_as_uint(fmaf(w1, 32768.0f, 8388608.0f)) * 65535u + kWordBias;
+            const uint32_t Wd =
+                REC ? Wrec : __float_as_uint(fmaf(w1, 32768.0f, 8388608.0f)) * 65535u + kWordBias;
             uint32_t wd[8];
             if constexpr (IDPM == 1) {  // pair lines: the words are in shared memory as they are
               const uint8_t* qp = Tq + (k * L + l0) * PLINE;
@@ -1055,9 +1081,9 @@ __global__ void idp_bound_kernel(const uint8_t* q, const float* scale, const flo
 }
 
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1, bool GC = false,
-          bool BAL = false, int XB = 1, bool XT = false, int IDPM = 0>
+          bool BAL = false, int XB = 1, bool XT = false, int IDPM = 0, bool REC = false>
 void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
-  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, IDPM>;
+  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, IDPM, REC>;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -1072,7 +1098,13 @@ void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
 // are never used with codes in global memory.
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1, bool GC = false,
           bool BAL = false, int XB = 1, bool XT = false>
-void launch_idp(int idp, cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
+void launch_idp(int idp, cudaStream_t st, const TiledArgs& a, size_t smem, int grid, bool rec = false) {
+  if constexpr (XT) {
+    if (rec) {  // coordinate records (coord_pass_kernel) over the standard lines
+      launch_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, 2, true>(st, a, smem, grid);
+      return;
+    }
+  }
   if (idp == 2) {
     launch_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, 2>(st, a, smem, grid);
     return;
@@ -1434,8 +1466,63 @@ __global__ void transpose_kernel(const float* __restrict__ X, int64_t rows, int3
   }
 }
 
+// Coordinate records (REC walk): the per-(row, input) half of the table walk — finite check, mask,
+// clip, segment, sample index and integer lerp weight (coords.cuh fast path with its exact fallback,
+// i.e. exactly what the walk computes in registers) plus the base activation silu(x') in f64 —
+// done ONCE per input element instead of once per j-block, written transposed ([d][ld] with the
+// row count padded to 4 for the tensor maps) next to each other:
+//   Rt: W1 (bits 0-14, W1 = round(w1 * 2^15); 2^15 moves to the next sample with W1 = 0, the same
+//       integer lerp) | code line k*L + l0 (bits 15-27) | out of range (bit 31);
+//   St: silu(zero_spline ? x : x').
+struct CoordPassArgs {
+  lkg::CoordConst cc;
+  float4 ktab[kMaxKT];
+};
+
+__global__ void coord_pass_kernel(const __grid_constant__ CoordPassArgs c, const float* __restrict__ X, int64_t rows,
+                                  int32_t d, int64_t ld, uint32_t* __restrict__ Rt, float* __restrict__ St, int zs,
+                                  unsigned long long* nonfinite) {
+  __shared__ float t[32][33];
+  __shared__ float4 ktab[kMaxKT];
+  __shared__ float2 kf[kMaxKT];
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int q = tid; q < c.cc.K; q += 32 * blockDim.y) {
+    ktab[q] = c.ktab[q];
+    kf[q] = make_float2(c.ktab[q].x, c.ktab[q].y);
+  }
+  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  const int c0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t r = r0 + k;
+    const int col = c0 + threadIdx.x;
+    if (r < rows && col < d) t[k][threadIdx.x] = X[r * d + col];
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int col = c0 + k;
+    const int64_t r = r0 + threadIdx.x;
+    if (r < rows && col < d) {
+      const float v = t[threadIdx.x][k];
+      bad |= !(fabsf(v) <= 3.402823466e38f);  // runtime.cpp:172 (NaN and inf)
+      const lkg::Coord co = lkg::lut_coords_fast(c.cc, ktab, kf, v);
+      uint32_t w1 = __float_as_uint(fmaf(co.w1, 32768.0f, 8388608.0f)) - 0x4B000000u;
+      int l0 = co.l0;
+      if (w1 >= 32768u) {
+        w1 = 0u;
+        l0 += 1;
+      }
+      const uint32_t line = (uint32_t)(co.k * c.cc.L + l0);
+      Rt[(int64_t)col * ld + r] = w1 | (line << 15) | (co.in ? 0u : 0x80000000u);
+      St[(int64_t)col * ld + r] = lkg::silu_exact(zs ? v : co.xp);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && threadIdx.x == 0) atomicExch(nonfinite, 1ull);
+}
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency)
-static void encode_x_map(CUtensorMap* map, const float* Xt, int64_t rows, int d, int box_rows, int box_cols) {
+static void encode_x_map(CUtensorMap* map, const float* Xt, int64_t rows, int d, int box_rows, int box_cols,
+                         int64_t ld = 0) {
   typedef CUresult (*Encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1446,7 +1533,7 @@ static void encode_x_map(CUtensorMap* map, const float* Xt, int64_t rows, int d,
     if (!enc || q != cudaDriverEntryPointSuccess) throw Error{LKG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable"};
   }
   const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)d};
-  const cuuint64_t strides[1] = {(cuuint64_t)rows * sizeof(float)};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld > 0 ? ld : rows) * sizeof(float)};
   const cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols}, es[2] = {1u, 1u};
   if (enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(Xt), dims, strides, box, es,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1509,19 +1596,40 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   // codes-in-L2 (GC) layers take XT too when they have f64 accumulators (C5 layer 0: -4.4 % time;
   // the row-major x staging shares L1 with the __ldg code reads there)
   const bool xt_gc_ok = f64;
-  const bool xt = !(xt_env && xt_env[0] == '0') && (!gm.codes_global || xt_gc_ok) && !L2 && gm.n_jb >= 16 &&
-                  x_blk <= 0 && rows % row_tile == 0 && L->in_dim % G == 0 && rows < (1ll << 31);
+  // REC: layers with several j-blocks on the integer-lerp walk get their coordinates once per input
+  // element from coord_pass_kernel (transposed records + silu, TMA boxes like XT): the walk keeps
+  // only the table work. Any row count and input width (the boxes past the ends are zero records,
+  // which are in range and hit zero P entries). LKG_REC=0 disables (A/B hook).
+  static const char* rec_env = getenv("LKG_REC");
+  const int Ls = L->L;
+  const bool rec = !(rec_env && rec_env[0] == '0') && gm.idp == 2 && (Ls & (Ls - 1)) == 0 && L->K * Ls <= 8192 &&
+                   !L2 && x_blk <= 0 && gm.n_jb >= 4 && rows > 0 && rows < (1ll << 31) &&
+                   (!gm.codes_global || xt_gc_ok);
+  const bool xt = rec || (!(xt_env && xt_env[0] == '0') && (!gm.codes_global || xt_gc_ok) && !L2 && gm.n_jb >= 16 &&
+                          x_blk <= 0 && rows % row_tile == 0 && L->in_dim % G == 0 && rows < (1ll << 31));
   if (xt) {
-    const size_t xt_elems = (size_t)rows * L->in_dim;
+    const int64_t ld = (rows + 3) / 4 * 4;  // 16-byte tensor-map strides
+    const size_t xt_elems = (size_t)ld * L->in_dim;
     if (ctx->xt.bytes < 2 * sizeof(float) * xt_elems) ctx->xt.alloc(2 * sizeof(float) * xt_elems);
     float* Xt = ctx->xt.as<float>();
     float* St = Xt + xt_elems;
-    transpose_kernel<<<dim3((unsigned)((rows + 31) / 32), (unsigned)((L->in_dim + 31) / 32)), dim3(32, 8), 0,
-                       ctx->stream>>>(X, rows, L->in_dim, Xt, St, a.cc.lo, a.cc.hi_clip, zs);
+    const dim3 tgrid((unsigned)((rows + 31) / 32), (unsigned)((L->in_dim + 31) / 32));
+    if (rec) {
+      CoordPassArgs ca{};
+      ca.cc = a.cc;
+      for (int k = 0; k < a.cc.K; k++) ca.ktab[k] = a.ktab[k];
+      coord_pass_kernel<<<tgrid, dim3(32, 8), 0, ctx->stream>>>(ca, X, rows, L->in_dim, ld,
+                                                               reinterpret_cast<uint32_t*>(Xt), St, zs,
+                                                               a.counters + 2);
+      a.lgL = __builtin_ctz((unsigned)Ls);
+    } else {
+      transpose_kernel<<<tgrid, dim3(32, 8), 0, ctx->stream>>>(X, rows, L->in_dim, Xt, St, a.cc.lo, a.cc.hi_clip,
+                                                               zs);
+    }
     LKG_CUDA(cudaGetLastError());
     ctx->launches++;
-    encode_x_map(&a.xmap, Xt, rows, L->in_dim, 32 * R, G);
-    encode_x_map(&a.smap, St, rows, L->in_dim, 32 * R, G);
+    encode_x_map(&a.xmap, Xt, rows, L->in_dim, 32 * R, G, ld);
+    encode_x_map(&a.smap, St, rows, L->in_dim, 32 * R, G, ld);
     a.X = Xt;
     smem += (size_t)W * G * (32 * R) * 4;  // the silu boxes
     switch (sel) {
@@ -1529,13 +1637,13 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   case S:                                                                                                      \
     if (f64 && gm.codes_global)                                                                                \
       launch_idp<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, true, false, 1, true>(       \
-          gm.idp, ctx->stream, a, smem, grid);                                                                         \
+          gm.idp, ctx->stream, a, smem, grid, rec);                                                                         \
     else if (f64)                                                                                              \
       launch_idp<kR64, kW64, (S >> 2) & 1, (S >> 1) & 1, S & 1, true, false, 1, false, false, 1, true>(      \
-          gm.idp, ctx->stream, a, smem, grid);                                                                         \
+          gm.idp, ctx->stream, a, smem, grid, rec);                                                                         \
     else                                                                                                       \
       launch_idp<kR, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, false, 1, true>(         \
-          gm.idp, ctx->stream, a, smem, grid);                                                                         \
+          gm.idp, ctx->stream, a, smem, grid, rec);                                                                         \
     break;
       CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE

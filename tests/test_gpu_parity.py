@@ -798,3 +798,37 @@ def test_transposed_input_walk_codes_in_l2_bit_identical(lk, oracle):
     ao = oracle.compile_layer(to_oracle_spec(lk.recipe_layer(5, 0, c0, c1)), 128, 1, 1, 0, 1, 1)
     Yo, _ = oracle.lut_forward(ao, X[2016:2048].astype(np.float64), nthreads=8)
     assert_close(Yt[2016:2048, c0:c1], Yo, "GC XT walk vs oracle")
+
+
+@pytest.mark.gpu
+def test_coordinate_record_walk(lk, oracle, tmp_path):
+    """Layers with >= 4 j-blocks on the integer-lerp walk take their coordinates once per input
+    element from the coordinate pass (REC): bit-identical to the in-kernel coordinates where both
+    read the same silu boxes (XT, f64 accumulators: a 1024 -> 1024 layer on 2048 rows), and within the
+    bar against the reference on ragged shapes the pass allows (row counts not a multiple of 1024,
+    input widths not a multiple of 8)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = (
+        "import sys, numpy as np, torch; sys.path[:0] = [%r, %r]\n"
+        "import paper_2601_03332_b200 as lk\n"
+        "a = lk.compile_layer(lk.gen_layer(5, 1024, 1024, 8), lk.QuantConfig(64),"
+        " lk.OobConfig(lk.BoundaryMode.HalfOpen, lk.OobPolicy.ClipX))\n"
+        "X = torch.from_numpy(np.random.default_rng(3).uniform(-1.3, 1.3, (2048, 1024)).astype(np.float32)).cuda()\n"
+        "Y, st = lk.lut_layer_forward_batch(a, X)\n"
+        "np.save(%r + '/y.npy', Y.cpu().numpy()); np.save(%r + '/s.npy', np.array([st.n_oob_inputs, st.n_oob_samples]))\n"
+    ) % (os.path.dirname(here), here, str(tmp_path), str(tmp_path))
+    outs = {}
+    for rec in ("1", "0"):
+        subprocess.run([sys.executable, "-c", code], env=dict(os.environ, LKG_REC=rec), check=True)
+        outs[rec] = (np.load(tmp_path / "y.npy"), np.load(tmp_path / "s.npy"))
+    assert np.array_equal(outs["1"][0], outs["0"][0]) and np.array_equal(outs["1"][1], outs["0"][1])
+    # ragged shapes through the pass, against the reference
+    for d, m, rows, contract in ((300, 64, 777, (0, 0)), (60, 128, 1999, (1, 1)), (64, 64, 2501, (0, 1))):
+        so = oracle.gen_layer(17 + d, d, m, 8)
+        for scheme in (0, 1):
+            art = oracle.compile_layer(so, 64, scheme, 1, 0, *contract)
+            X = np.random.default_rng(d + m).uniform(-1.4, 1.4, (rows, d)).astype(np.float32)
+            _layer_parity(lk, oracle, art, X, f"REC d{d} m{m} rows{rows} scheme{scheme}")
