@@ -595,6 +595,16 @@ static void run_chain(lkg_ctx* ctx, const lkg_layer* const* chain, int n, const 
     if (chain[l]->in_dim != chain[l - 1]->out_dim)
       fail(LKG_ERR_DIMENSION, "artifact chain dimension mismatch between layers " + std::to_string(l - 1) +
                                   " and " + std::to_string(l));
+  if (rows > 0 && lkg::can_fuse_chain(chain, n)) {
+    // every layer is a small value-table layer: the whole chain in one launch (forward_chain.cu),
+    // hidden activations stay in the row's thread
+    lkg::launch_forward_chain(ctx, chain, n, X, rows, Y);
+    for (int s = 0; s < n; s++) {
+      ctx->rows_seen[s] += (uint64_t)rows;
+      ctx->in_dim_seen[s] = chain[s]->in_dim;
+    }
+    return;
+  }
   size_t hid = 0;
   for (int l = 0; l + 1 < n; l++) hid = std::max(hid, (size_t)chain[l]->out_dim);
   if (n > 1) {

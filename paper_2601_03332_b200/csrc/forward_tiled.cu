@@ -128,6 +128,21 @@ using lkg::mbar_wait;
 // matters: L1::no_allocate measured 1.6x slower, L1::evict_last no different.
 __device__ __forceinline__ uint4 gc_load(const uint8_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 
+// GC pair entries (IDPM == 3, codes in global memory): per (input, segment, sample) one 32-byte
+// entry holding the 16 outputs' codes of sample l NEXT TO those of sample l+1, already in dp2a word
+// order [u_l(j), u_l+1(j), u_l(j+1), u_l+1(j+1)] — a (row, input) is ONE 256-bit load of one sector
+// (the standard lines cost two 16-byte loads from two 128-byte lines plus 8 PRMT). Entries are
+// input-major inside a tile: [8 i_lo][K][L][32 B]; sample L-1's successor slot is 0 (its weight is 0).
+constexpr int GCE = 32;
+__host__ __device__ __forceinline__ int64_t gce_off(int il, int k, int l, int K, int L) {
+  return ((int64_t)(il * K + k) * L + l) * GCE;
+}
+__device__ __forceinline__ void gc_load256(const uint8_t* p, uint32_t (&w)[8]) {
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+               : "l"(p));
+}
+
 __device__ __forceinline__ float magic(uint32_t w, uint32_t sel) {
   return __uint_as_float(__byte_perm(w, 0x4B000000u, sel));  // 2^23 + byte
 }
@@ -399,7 +414,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
 #pragma unroll 1
       for (int s = 0; s < n_steps; s++) {
         const int il = (s + lane) & 7;
-        const uint8_t* Tq = Tcodes + (IDPM == 1 ? pair_off(il, 0, 0) : il * JB);
+        const uint8_t* Tq = Tcodes + (IDPM == 3 ? gce_off(il, 0, 0, K, L) : IDPM == 1 ? pair_off(il, 0, 0) : il * JB);
         const uint8_t* Tp = T + a.p_off + il * PROW;
         // ---- steps 1-4 (runtime.cpp:170-190): mask, clip, segment, coordinates (coords.cuh),
         // the R rows' fast chains side by side, then the exact path once for any that need it
@@ -466,8 +481,10 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           LKG_DCHECK(prow >= 0 && prow <= K * G * PROW, "P row out of the staged block");
           LKG_DCHECK(GC || (int64_t)(k * L + l0 + 1) * (IDPM == 1 ? PLINE : LINE) + LINE <= a.p_off,
                      "code line past the staged code block");
-          LKG_DCHECK(!GC || ((int64_t)jb * a.n_ih + ih) * tb + (int64_t)(k * L + l0 + 2) * LINE <= a.tiles_bytes,
+          LKG_DCHECK(!GC || IDPM == 3 ||
+                         ((int64_t)jb * a.n_ih + ih) * tb + (int64_t)(k * L + l0 + 2) * LINE <= a.tiles_bytes,
                      "code line past the layer's tiles (GC)");
+          LKG_DCHECK(IDPM != 3 || gce_off(il, k, l0, K, L) + GCE <= a.p_off, "pair entry past the tile's code block (GC)");
           LKG_DCHECK(st >= 0 && st < NS, "stage index");
           (void)xp;
           if constexpr (IDPM != 0) {
@@ -477,7 +494,9 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
             const uint32_t Wd =
                 REC ? Wrec : __float_as_uint(fmaf(w1, 32768.0f, 8388608.0f)) * 65535u + kWordBias;
             uint32_t wd[8];
-            if constexpr (IDPM == 1) {  // pair lines: the words are in shared memory as they are
+            if constexpr (IDPM == 3) {  // GC pair entries: one 256-bit read-only load, words as stored
+              gc_load256(Tq + (k * L + l0) * GCE, wd);
+            } else if constexpr (IDPM == 1) {  // pair lines: the words are in shared memory as they are
               const uint8_t* qp = Tq + (k * L + l0) * PLINE;
               // Tq points at half 0 (chunk il >> 2 of the input's 32 bytes); half 1 is the other chunk
               const uint4 h0 = *reinterpret_cast<const uint4*>(qp);
@@ -1040,7 +1059,13 @@ __global__ void build_tiles_kernel(const uint8_t* q, const float* scale, const f
   const int ih = i / G, il = i % G, jb = j / JB, jl = j % JB;
   uint8_t* t = tiles + ((int64_t)jb * n_ih + ih) * tile_bytes;
   const uint8_t* src = q + cell * L;
-  if (idp == 1) {
+  if (idp == 3) {
+    for (int l = 0; l < L; l++) {
+      uint8_t* ent = t + gce_off(il, k, l, K, L) + (jl >> 1) * 4 + (jl & 1) * 2;
+      ent[0] = sym ? (uint8_t)(src[l] ^ 0x80u) : src[l];
+      ent[1] = l + 1 < L ? (sym ? (uint8_t)(src[l + 1] ^ 0x80u) : src[l + 1]) : 0;
+    }
+  } else if (idp == 1) {
     for (int l = 0; l < L; l++) {
       uint8_t* line = t + (int64_t)(k * L + l) * PLINE;
       line[pair_off(il, jl, 0)] = sym ? (uint8_t)(src[l] ^ 0x80u) : src[l];
@@ -1100,8 +1125,20 @@ template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false
           bool BAL = false, int XB = 1, bool XT = false>
 void launch_idp(int idp, cudaStream_t st, const TiledArgs& a, size_t smem, int grid, bool rec = false) {
   if constexpr (XT) {
-    if (rec) {  // coordinate records (coord_pass_kernel) over the standard lines
+    if (rec) {  // coordinate records (coord_pass_kernel) over the standard lines / the GC pair entries
+      if constexpr (GC) {
+        if (idp == 3) {
+          launch_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, 3, true>(st, a, smem, grid);
+          return;
+        }
+      }
       launch_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, 2, true>(st, a, smem, grid);
+      return;
+    }
+  }
+  if constexpr (GC) {
+    if (idp == 3) {  // pair entries in global memory
+      launch_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, 3>(st, a, smem, grid);
       return;
     }
   }
@@ -1229,7 +1266,9 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   }
   const size_t xs_bytes = (size_t)1 * kW * G * (32 * kR + 4) * 4;  // one x buffer (fwd_tiled XB)
   auto layout = [&](int mode) {  // tile offsets for the given code layout; returns the tile bytes
-    int64_t o = mode == 1 ? (int64_t)K * Ls * PLINE : (int64_t)(K * Ls + 1) * LINE;
+    int64_t o = mode == 3   ? (int64_t)K * Ls * G * GCE
+                : mode == 1 ? (int64_t)K * Ls * PLINE
+                            : (int64_t)(K * Ls + 1) * LINE;
     gm.p_off = (int32_t)o;
     o += (int64_t)(K + 1) * G * PROW;
     if (asym) {
@@ -1252,6 +1291,27 @@ void build_tiles(lkg_ctx* ctx, lkg_layer* L) {
   gm.idp = idp;
   gm.codes_global = force_gc || 2 * off + xs_bytes + kMaxKT * 32 + 256 > 227 * 1024;  // codes stay in global (L2)
   if (gm.codes_global && 2 * (off - gm.p_off) + xs_bytes + kMaxKT * 32 + 256 > 227 * 1024) return;  // generic
+  // Codes in global memory on the integer-lerp walk: pair entries (twice the code bytes; one 256-bit
+  // load of one sector per (row, input) instead of two 16-byte loads from two lines plus 8 PRMT — the
+  // walk was L1TEX-bound on sectors) when the device has room for them. LKG_GCPAIR=0 keeps the lines.
+  if (gm.codes_global && idp == 2) {
+    static const char* gp = getenv("LKG_GCPAIR");
+    const int64_t off3 = layout(3);
+    size_t mfree = 0, mtotal = 0;
+    LKG_CUDA(cudaMemGetInfo(&mfree, &mtotal));
+    const size_t need = (size_t)((d + G - 1) / G) * ((m + JB - 1) / JB) * (size_t)off3;
+    // Only where a tile's code lines outgrow L1 anyway (configs[4]: 262 KB per tile, measured 162.5 ->
+    // 148.9 ms per layer); a tile that L1 holds (configs[2] at L=128: 131 KB) is faster on the lines
+    // (0.466 vs 0.532 ms: the doubled bytes halve its L1 hit rate). LKG_GCPAIR=1 forces the entries.
+    const bool big = (int64_t)(K * Ls + 1) * LINE > 192 * 1024 || (gp && gp[0] == '1');
+    if (!(gp && gp[0] == '0') && big && need + (4ull << 30) <= mfree) {
+      idp = 3;
+      gm.idp = 3;
+      off = off3;
+    } else {
+      off = layout(0);  // (restores the offsets of the standard lines)
+    }
+  }
   gm.tile_bytes = off;
   gm.JB = JB;
   gm.IC = G;
@@ -1284,8 +1344,10 @@ __global__ void tiles_to_q_kernel(const uint8_t* tiles, int64_t tile_bytes, int3
   const int i = i0 + (int)(e / m), j = (int)(e % m);
   const uint8_t* t = tiles + ((int64_t)(j / JB) * n_ih + i / G) * tile_bytes;
   for (int l = 0; l < L; l++) {
-    const uint8_t b = idp == 1 ? t[(int64_t)(k * L + l) * PLINE + pair_off(i % G, j % JB, 0)]
-                               : t[(k * L + l) * LINE + (i % G) * JB + (j % JB)];
+    const int jl = j % JB;
+    const uint8_t b = idp == 3   ? t[gce_off(i % G, k, l, K, L) + (jl >> 1) * 4 + (jl & 1) * 2]
+                      : idp == 1 ? t[(int64_t)(k * L + l) * PLINE + pair_off(i % G, jl, 0)]
+                                 : t[(k * L + l) * LINE + (i % G) * JB + jl];
     q[cell * L + l] = sym ? (uint8_t)(b ^ 0x80u) : b;
   }
 }
@@ -1445,7 +1507,7 @@ bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
 // base-branch activations St = silu(zs ? x : clamp(x, t_0, hi_clip)) in the same layout (f64, one
 // rounding to f32: each element once, instead of once per j-block inside the table walk).
 __global__ void transpose_kernel(const float* __restrict__ X, int64_t rows, int32_t d, float* __restrict__ Xt,
-                                 float* __restrict__ St, float lo, float hi_clip, int zs) {
+                                 float* __restrict__ St, float lo, float hi_clip, int zs, int exact) {
   __shared__ float t[32][33];
   const int64_t r0 = (int64_t)blockIdx.x * 32;
   const int c0 = blockIdx.y * 32;
@@ -1461,7 +1523,8 @@ __global__ void transpose_kernel(const float* __restrict__ X, int64_t rows, int3
     if (r < rows && c < d) {
       const float v = t[threadIdx.x][k];
       Xt[(int64_t)c * rows + r] = v;
-      St[(int64_t)c * rows + r] = lkg::silu_exact(zs ? v : fminf(fmaxf(v, lo), hi_clip));
+      const float xb = zs ? v : fminf(fmaxf(v, lo), hi_clip);
+      St[(int64_t)c * rows + r] = exact ? lkg::silu_exact(xb) : lkg::silu_fast(xb);
     }
   }
 }
@@ -1481,7 +1544,7 @@ struct CoordPassArgs {
 
 __global__ void coord_pass_kernel(const __grid_constant__ CoordPassArgs c, const float* __restrict__ X, int64_t rows,
                                   int32_t d, int64_t ld, uint32_t* __restrict__ Rt, float* __restrict__ St, int zs,
-                                  unsigned long long* nonfinite) {
+                                  int exact, unsigned long long* nonfinite) {
   __shared__ float t[32][33];
   __shared__ float4 ktab[kMaxKT];
   __shared__ float2 kf[kMaxKT];
@@ -1514,7 +1577,9 @@ __global__ void coord_pass_kernel(const __grid_constant__ CoordPassArgs c, const
       }
       const uint32_t line = (uint32_t)(co.k * c.cc.L + l0);
       Rt[(int64_t)col * ld + r] = w1 | (line << 15) | (co.in ? 0u : 0x80000000u);
-      St[(int64_t)col * ld + r] = lkg::silu_exact(zs ? v : co.xp);
+      // the walk's own base activation: f64 for the f64-accumulating layers, MUFU otherwise (so a
+      // layer keeps its result bits whether or not it takes the coordinate pass, e.g. column shards)
+      St[(int64_t)col * ld + r] = exact ? lkg::silu_exact(zs ? v : co.xp) : lkg::silu_fast(zs ? v : co.xp);
     }
   }
   if (__any_sync(0xffffffffu, bad) && threadIdx.x == 0) atomicExch(nonfinite, 1ull);
@@ -1602,7 +1667,7 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   // which are in range and hit zero P entries). LKG_REC=0 disables (A/B hook).
   static const char* rec_env = getenv("LKG_REC");
   const int Ls = L->L;
-  const bool rec = !(rec_env && rec_env[0] == '0') && gm.idp == 2 && (Ls & (Ls - 1)) == 0 && L->K * Ls <= 8192 &&
+  const bool rec = !(rec_env && rec_env[0] == '0') && (gm.idp == 2 || gm.idp == 3) && (Ls & (Ls - 1)) == 0 && L->K * Ls <= 8192 &&
                    !L2 && x_blk <= 0 && gm.n_jb >= 4 && rows > 0 && rows < (1ll << 31) &&
                    (!gm.codes_global || xt_gc_ok);
   const bool xt = rec || (!(xt_env && xt_env[0] == '0') && (!gm.codes_global || xt_gc_ok) && !L2 && gm.n_jb >= 16 &&
@@ -1619,12 +1684,12 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
       ca.cc = a.cc;
       for (int k = 0; k < a.cc.K; k++) ca.ktab[k] = a.ktab[k];
       coord_pass_kernel<<<tgrid, dim3(32, 8), 0, ctx->stream>>>(ca, X, rows, L->in_dim, ld,
-                                                               reinterpret_cast<uint32_t*>(Xt), St, zs,
+                                                               reinterpret_cast<uint32_t*>(Xt), St, zs, f64,
                                                                a.counters + 2);
       a.lgL = __builtin_ctz((unsigned)Ls);
     } else {
       transpose_kernel<<<tgrid, dim3(32, 8), 0, ctx->stream>>>(X, rows, L->in_dim, Xt, St, a.cc.lo, a.cc.hi_clip,
-                                                               zs);
+                                                               zs, f64);
     }
     LKG_CUDA(cudaGetLastError());
     ctx->launches++;

@@ -150,6 +150,9 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
                           int slot, const lkg_layer* L2 = nullptr, float* Y2 = nullptr);
 // True when layer L2 (small out_dim, whole LUT in smem) can run in L1's epilogue (chain fusion).
 bool can_fuse(const lkg_layer* L1, const lkg_layer* L2);
+// Whole-chain fusion (forward_chain.cu): every layer a small value-table layer, one launch.
+bool can_fuse_chain(const lkg_layer* const* chain, int n);
+void launch_forward_chain(lkg_ctx* ctx, const lkg_layer* const* chain, int n, const float* X, int64_t rows, float* Y);
 // Reference-layout q_table of a layer whose codes live only in its tiles.
 void download_q_from_tiles(lkg_ctx* ctx, const lkg_layer* L, uint8_t* host_q);
 // One layer forward. X has row stride x_ld and, when x_blk > 0, is stored as rank-major

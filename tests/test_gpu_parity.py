@@ -254,6 +254,70 @@ def test_chain_c1(lk, oracle):
     assert np.array_equal(r.Y, Y2)
 
 
+def test_gc_pair_entries_bit_identical(tmp_path):
+    """Codes-in-global layers on the integer-lerp walk can store pair entries (one 256-bit load per
+    (row, input), chosen for tiles beyond L1: configs[4]); forced here (LKG_GCPAIR=1) on the C3 L=128
+    layer in both schemes: the same output bits and OobStats as the code lines (LKG_GCPAIR=0), and the
+    reference-layout q_table rebuilt from the pair entries byte for byte (tiles-only download)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = (
+        "import sys, numpy as np; sys.path[:0] = [%r, %r]\n"
+        "import paper_2601_03332_b200 as lk\n"
+        "X = lk.recipe_inputs(3, 0, 3001)\n"
+        "for s in (0, 1):\n"
+        "    a = lk.compile_layer(lk.recipe_layer(3, 0), lk.QuantConfig(128, lk.Scheme(s), lk.Dtype(s)),"
+        " lk.OobConfig(lk.BoundaryMode.Closed, lk.OobPolicy(s)))\n"
+        "    Y, st = lk.lut_layer_forward_batch(a, X)\n"
+        "    np.save(%r + '/y%%d.npy' %% s, Y); np.save(%r + '/q%%d.npy' %% s, a.q_table)\n"
+        "    np.save(%r + '/s%%d.npy' %% s, np.array([st.n_oob_samples, st.n_oob_inputs]))\n"
+    ) % (os.path.dirname(here), here, str(tmp_path), str(tmp_path), str(tmp_path))
+    outs = {}
+    for pair in ("1", "0"):
+        subprocess.run([sys.executable, "-c", code], check=True,
+                       env=dict(os.environ, LKG_GCPAIR=pair, LKG_TILE_ONLY_BYTES="0"))
+        outs[pair] = [[np.load(tmp_path / f"{n}{s}.npy") for n in "yqs"] for s in (0, 1)]
+    for s in (0, 1):
+        for a, b in zip(outs["1"][s], outs["0"][s]):
+            assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dims,rows,scheme,bm,op", [((2, 5, 1), 4096, 0, 0, 0), ((7, 8, 3, 2), 4097, 1, 1, 1),
+                                                    ((30, 4, 8, 4, 1), 63, 0, 1, 0), ((2, 5, 1), 1, 0, 0, 1),
+                                                    ((12, 6, 2), 400_000, 1, 0, 0)])
+def test_fused_small_chain(lk, oracle, dims, rows, scheme, bm, op):
+    """Chains whose every layer is a small value-table layer run as ONE launch (forward_chain.cu,
+    SURVEY §8f rank 3; the reference chain runtime.cpp:298-314): outputs and per-layer OobStats are
+    bit-identical to the layer-by-layer launches, the last layer is within the bar of the reference
+    on the GPU's own hidden values, and a non-finite hidden or input value raises NonFiniteError."""
+    eng = lk.Engine(0)
+    specs_o = [oracle.gen_layer(100 + l + sum(dims), dims[l], dims[l + 1], 5 + l) for l in range(len(dims) - 1)]
+    Ls = 64 if dims[0] == 2 else 16   # (all the value tables must fit shared memory together)
+    chain_o = [oracle.compile_layer(s, Ls, scheme, 1, 0, bm, op) for s in specs_o]
+    chain = [to_product_artifact(lk, a) for a in chain_o]
+    X = np.random.default_rng(rows).uniform(-1.3, 1.3, (rows, dims[0])).astype(np.float32)
+    lk.lut_model_forward_batch(chain, X[:1], engine=eng)        # (uploads the artifacts)
+    n0 = eng.launch_count
+    r = lk.lut_model_forward_batch(chain, X, engine=eng)
+    assert eng.launch_count - n0 == 1                          # one kernel for the whole chain
+    H, per_layer = X, []
+    for l, a in enumerate(chain):                              # layer by layer: never fused
+        Hn, st = lk.lut_layer_forward_batch(a, H, engine=eng)
+        per_layer.append(stats_list(st))
+        if l == len(chain) - 1:
+            Yo, _ = oracle.lut_forward(chain_o[l], H.astype(np.float64))
+            assert_close(r.Y, Yo, f"fused chain {dims} last layer")
+        H = Hn
+    assert np.array_equal(r.Y, H)
+    assert [stats_list(s) for s in r.per_layer] == per_layer
+    Xn = X.copy()
+    Xn[rows // 2, 0] = np.nan
+    with pytest.raises(lk.NonFiniteError):
+        lk.lut_model_forward_batch(chain, Xn, engine=eng)
+
+
 # ------------------------------------------------------------------ spline
 @pytest.mark.parametrize("cfg,layer,rows", [(1, 0, 4096), (2, 0, 4000), (3, 0, 2000), (4, 2, 256)])
 def test_spline_forward(lk, oracle, cfg, layer, rows):
@@ -819,12 +883,17 @@ def test_coordinate_record_walk(lk, oracle, tmp_path):
         "X = torch.from_numpy(np.random.default_rng(3).uniform(-1.3, 1.3, (2048, 1024)).astype(np.float32)).cuda()\n"
         "Y, st = lk.lut_layer_forward_batch(a, X)\n"
         "np.save(%r + '/y.npy', Y.cpu().numpy()); np.save(%r + '/s.npy', np.array([st.n_oob_inputs, st.n_oob_samples]))\n"
-    ) % (os.path.dirname(here), here, str(tmp_path), str(tmp_path))
+        # an fp32-accumulating layer (C3 layer 0, 4 j-blocks): the pass takes the walk's own MUFU silu
+        "b = lk.compile_layer(lk.recipe_layer(3, 0), lk.QuantConfig(64), lk.OobConfig())\n"
+        "Y2, _ = lk.lut_layer_forward_batch(b, torch.from_numpy(lk.recipe_inputs(3, 0, 3000)).cuda())\n"
+        "np.save(%r + '/y2.npy', Y2.cpu().numpy())\n"
+    ) % (os.path.dirname(here), here, str(tmp_path), str(tmp_path), str(tmp_path))
     outs = {}
     for rec in ("1", "0"):
         subprocess.run([sys.executable, "-c", code], env=dict(os.environ, LKG_REC=rec), check=True)
-        outs[rec] = (np.load(tmp_path / "y.npy"), np.load(tmp_path / "s.npy"))
+        outs[rec] = (np.load(tmp_path / "y.npy"), np.load(tmp_path / "s.npy"), np.load(tmp_path / "y2.npy"))
     assert np.array_equal(outs["1"][0], outs["0"][0]) and np.array_equal(outs["1"][1], outs["0"][1])
+    assert np.array_equal(outs["1"][2], outs["0"][2])
     # ragged shapes through the pass, against the reference
     for d, m, rows, contract in ((300, 64, 777, (0, 0)), (60, 128, 1999, (1, 1)), (64, 64, 2501, (0, 1))):
         so = oracle.gen_layer(17 + d, d, m, 8)
