@@ -136,6 +136,13 @@ lkg_status lkg_ctx_synchronize(lkg_ctx* ctx);
 void* lkg_ctx_stream(lkg_ctx* ctx);
 /* Number of kernels this context has launched so far (for bench's gpu_launches). */
 uint64_t lkg_ctx_launch_count(lkg_ctx* ctx);
+/* Device workspace the context holds between calls: hidden-activation ping-pong buffers, the
+ * transposed-input / coordinate-record buffer of the wide-layer table walk (2 x rows x in_dim x 4 B,
+ * e.g. 8.6 GB after a configs[3] batch), the sharded chain's gather buffer and the host entries'
+ * staging. Buffers grow on demand and are reused; lkg_ctx_trim synchronizes the stream and frees them
+ * (the reference's Matrix temporaries die with each call, runtime.cpp:298-314). */
+uint64_t lkg_ctx_workspace_bytes(lkg_ctx* ctx);
+lkg_status lkg_ctx_trim(lkg_ctx* ctx);
 
 /* -------------------------------------------------------- artifact (F1, F2) */
 /* Validates like LutLayerArtifact::finalize (runtime.cpp:11-43) and uploads. */

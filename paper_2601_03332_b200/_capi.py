@@ -70,6 +70,8 @@ SIGNATURES = {
     "lkg_ctx_synchronize": (C.c_int, [C.c_void_p]),
     "lkg_ctx_stream": (C.c_void_p, [C.c_void_p]),
     "lkg_ctx_launch_count": (C.c_uint64, [C.c_void_p]),
+    "lkg_ctx_workspace_bytes": (C.c_uint64, [C.c_void_p]),
+    "lkg_ctx_trim": (C.c_int, [C.c_void_p]),
     "lkg_layer_upload": (C.c_int, [C.c_void_p, _P(LayerDesc), _P(C.c_void_p)]),
     "lkg_layer_upload_columns": (C.c_int, [C.c_void_p, _P(LayerDesc), C.c_int32, C.c_int32, _P(C.c_void_p)]),
     "lkg_layer_info_get": (C.c_int, [C.c_void_p, _P(LayerInfo)]),

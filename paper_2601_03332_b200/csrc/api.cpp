@@ -249,6 +249,24 @@ lkg_status lkg_ctx_set_spline_kernel(lkg_ctx* ctx, int32_t kind) {
   });
 }
 uint64_t lkg_ctx_launch_count(lkg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+uint64_t lkg_ctx_workspace_bytes(lkg_ctx* ctx) {
+  if (!ctx) return 0;
+  return ctx->scratch[0].bytes + ctx->scratch[1].bytes + ctx->gather.bytes + ctx->hostio.bytes + ctx->xt.bytes;
+}
+lkg_status lkg_ctx_trim(lkg_ctx* ctx) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    DeviceGuard g(ctx->device);
+    LKG_CUDA(cudaStreamSynchronize(ctx->stream));  // no launch still reads the workspace
+    if (ctx->copy_stream) LKG_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    if (ctx->comm_stream) LKG_CUDA(cudaStreamSynchronize(ctx->comm_stream));
+    ctx->scratch[0].release();
+    ctx->scratch[1].release();
+    ctx->gather.release();
+    ctx->hostio.release();
+    ctx->xt.release();
+  });
+}
 
 // ------------------------------------------------------------------- layers
 static lkg_status upload_impl(lkg_ctx* ctx, const lkg_layer_desc* d, int32_t col0, int32_t col1,

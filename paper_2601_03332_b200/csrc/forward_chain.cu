@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "checks.cuh"
 #include "coords.cuh"
 #include "lkg_internal.h"
 #include "tma.cuh"
@@ -63,6 +64,9 @@ __device__ __forceinline__ void chain_layer(const ChainLayer& P, const float* V,
     const float* V0 = V + ((int64_t)(co.k * L + co.l0) * d + i) * ES;
     const float* V1 = P.vp ? V0 + MP : V0 + d * ES;
     const float* CB = CBt + i * MP;
+    LKG_DCHECK(co.k >= 0 && co.k < P.cc.K && co.l0 >= 0 && co.l0 < L && i >= 0 && i < d, "value-table index");
+    LKG_DCHECK((V1 - V + MP) * 4 <= P.cb_off, "value-table entry past the table");
+    LKG_DCHECK((i + 1) * MP * 4 + P.cb_off <= P.lut_bytes, "CB row past the layer image");
 #pragma unroll
     for (int j = 0; j < 8; j++) {
       if (j < MP) {

@@ -43,6 +43,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "checks.cuh"
 #include "coords.cuh"
 #include "lkg_internal.h"
 #include "tma.cuh"
@@ -52,25 +53,6 @@
 #define LKG_NS 2  // fwd_tiled stage buffers (see the kernel)
 #endif
 
-// LKG_CHECKS builds (tools/gpu/checks.sh) compile device-side bounds assertions into the table
-// walks: every shared-memory table index, staged-tile address, TMEM column and output coordinate is
-// checked against its allocation and the kernel traps with a message on the first violation.
-// (compute-sanitizer is closed on the GPU pool; these asserts plus canary buffers and repeat-launch
-// bit-identity tests are the memory/race evidence.)
-#ifdef LKG_CHECKS
-#define LKG_DCHECK(cond, what)                                                                          \
-  do {                                                                                                  \
-    if (!(cond)) {                                                                                      \
-      printf("LKG_CHECKS %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, threadIdx.x, \
-             what);                                                                                     \
-      __trap();                                                                                         \
-    }                                                                                                   \
-  } while (0)
-#else
-#define LKG_DCHECK(cond, what) \
-  do {                         \
-  } while (0)
-#endif
 
 namespace {
 
@@ -449,16 +431,17 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
         for (int r = 0; r < R; r++) {
           const float x = xv[r];
           bool in;
-          int k, l0;
+          int k, l0, cline;  // cline: the code line k*L + l0
           float xp, w1;
           uint32_t Wrec = 0;
           if constexpr (REC) {
             // record (coord_pass_kernel): W1 bits 0-14, code line k*L + l0 bits 15-27, OOB bit 31
+            // (the line is used as it is: re-forming it from k and l0 cost an IMAD and a LOP per row)
             const uint32_t rec = __float_as_uint(x);
             in = (rec >> 31) == 0u;
-            const int line = (int)((rec >> 15) & 0x1FFFu);
-            k = line >> a.lgL;
-            l0 = line & (L - 1);
+            cline = (int)((rec >> 15) & 0x1FFFu);
+            k = cline >> a.lgL;
+            l0 = cline & (L - 1);  // (bounds checks only)
             Wrec = (rec & 0x7FFFu) * 65535u + 32768u;
             xp = 0.0f;
             w1 = 0.0f;
@@ -469,6 +452,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
             l0 = co.l0;
             xp = co.xp;
             w1 = co.w1;  // w1: multiple of 2^-23 -> exact magic constants
+            cline = k * L + l0;
             nfacc = fmaf(x, 0.0f, nfacc);  // NaN once any input is NaN or inf
           }
           if (!in) {  // (predicated adds: cheaper than materialising the flag)
@@ -495,15 +479,15 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
                 REC ? Wrec : __float_as_uint(fmaf(w1, 32768.0f, 8388608.0f)) * 65535u + kWordBias;
             uint32_t wd[8];
             if constexpr (IDPM == 3) {  // GC pair entries: one 256-bit read-only load, words as stored
-              gc_load256(Tq + (k * L + l0) * GCE, wd);
+              gc_load256(Tq + cline * GCE, wd);
             } else if constexpr (IDPM == 1) {  // pair lines: the words are in shared memory as they are
-              const uint8_t* qp = Tq + (k * L + l0) * PLINE;
+              const uint8_t* qp = Tq + cline * PLINE;
               // Tq points at half 0 (chunk il >> 2 of the input's 32 bytes); half 1 is the other chunk
               const uint4 h0 = *reinterpret_cast<const uint4*>(qp);
               const uint4 h1 = *reinterpret_cast<const uint4*>(qp + 16 - ((il >> 2) << 5));
               wd[0] = h0.x, wd[1] = h0.y, wd[2] = h0.z, wd[3] = h0.w, wd[4] = h1.x, wd[5] = h1.y, wd[6] = h1.z, wd[7] = h1.w;
             } else {  // standard lines: pair each code with the next line's (one PRMT per 2 outputs)
-              const uint8_t* qp = Tq + (k * L + l0) * LINE;
+              const uint8_t* qp = Tq + cline * LINE;
               const uint4 c0 = GC ? gc_load(qp) : *reinterpret_cast<const uint4*>(qp);
               const uint4 c1 = GC ? gc_load(qp + LINE) : *reinterpret_cast<const uint4*>(qp + LINE);
               const uint32_t u0[4] = {c0.x, c0.y, c0.z, c0.w}, u1[4] = {c1.x, c1.y, c1.z, c1.w};
@@ -538,7 +522,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           }
           const float w0 = 1.0f - w1;
           const float cA = -fmaf(w0, M, OFF), cB = -w1 * M;
-          const uint8_t* qp = Tq + (k * L + l0) * LINE;
+          const uint8_t* qp = Tq + cline * LINE;
           const uint4 c0 = GC ? gc_load(qp) : *reinterpret_cast<const uint4*>(qp);
           const uint4 c1 = GC ? gc_load(qp + LINE) : *reinterpret_cast<const uint4*>(qp + LINE);
           const float2 W0 = make_float2(w0, w0), W1 = make_float2(w1, w1);

@@ -250,6 +250,16 @@ class Engine:
     def launch_count(self) -> int:
         return lib().lkg_ctx_launch_count(self.handle)
 
+    @property
+    def workspace_bytes(self) -> int:
+        """Device workspace held between calls (hidden activations, transposed inputs / coordinate
+        records, gather and staging buffers)."""
+        return lib().lkg_ctx_workspace_bytes(self.handle)
+
+    def trim(self) -> None:
+        """Synchronize and free the workspace (it regrows on demand)."""
+        check(lib().lkg_ctx_trim(self.handle))
+
     def collect(self, n_layers: int) -> list[OobStats]:
         arr = (_capi.OobStatsC * n_layers)()
         check(lib().lkg_ctx_collect(self.handle, arr, n_layers))

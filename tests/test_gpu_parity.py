@@ -254,6 +254,22 @@ def test_chain_c1(lk, oracle):
     assert np.array_equal(r.Y, Y2)
 
 
+def test_workspace_report_and_trim(lk):
+    """The context reports the device workspace it keeps between calls (hidden activations, the
+    coordinate-record buffer of the wide-layer walk) and frees it on request; it regrows on demand."""
+    eng = lk.Engine(0)
+    chain = lk.compile_model([lk.recipe_layer(3, l) for l in range(2)], lk.QuantConfig(64), lk.OobConfig(), engine=eng)
+    X = lk.recipe_inputs(3, 0, 3000)
+    assert eng.workspace_bytes == 0
+    r0 = lk.lut_model_forward_batch(chain, X, engine=eng)
+    # records + silu of the 64 -> 64 layer (2 x rows x 64 x 4 B) and the two hidden buffers (+ host staging)
+    assert eng.workspace_bytes >= 2 * 3000 * 64 * 4 + 2 * 3000 * 64 * 4
+    eng.trim()
+    assert eng.workspace_bytes == 0
+    r1 = lk.lut_model_forward_batch(chain, X, engine=eng)
+    assert np.array_equal(r0.Y, r1.Y)
+
+
 def test_gc_pair_entries_bit_identical(tmp_path):
     """Codes-in-global layers on the integer-lerp walk can store pair entries (one 256-bit load per
     (row, input), chosen for tiles beyond L1: configs[4]); forced here (LKG_GCPAIR=1) on the C3 L=128

@@ -28,7 +28,10 @@ def main():
     ch = lk.compile_model([lk.recipe_layer(1, l) for l in range(2)], lk.QuantConfig(64),
                           lk.OobConfig(lk.BoundaryMode.HalfOpen, lk.OobPolicy.ClipX))
     lk.lut_model_forward_batch(ch, Xc1)
-    print("C1 chain (fwd_small): ok", flush=True)
+    print("C1 chain (fwd_chain_small, one launch): ok", flush=True)
+    for a in ch:
+        Xc1, _ = lk.lut_layer_forward_batch(a, Xc1)
+    print("C1 layers (fwd_small): ok", flush=True)
     run("C2 layer 0 (fwd_tiled BAL, XB=2)", lk.recipe_layer(2, 0), torch.from_numpy(lk.recipe_inputs(2, 0, 3000)).cuda(),
         spline=True)
     X3 = torch.from_numpy(lk.recipe_inputs(3, 0, 2500)).cuda()
