@@ -251,7 +251,7 @@ lkg_status lkg_ctx_set_spline_kernel(lkg_ctx* ctx, int32_t kind) {
 uint64_t lkg_ctx_launch_count(lkg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 uint64_t lkg_ctx_workspace_bytes(lkg_ctx* ctx) {
   if (!ctx) return 0;
-  return ctx->scratch[0].bytes + ctx->scratch[1].bytes + ctx->gather.bytes + ctx->hostio.bytes + ctx->xt.bytes;
+  return ctx->scratch[0].bytes + ctx->scratch[1].bytes + ctx->gather.bytes + ctx->hostio.bytes + ctx->xt.bytes + ctx->ksp.bytes;
 }
 lkg_status lkg_ctx_trim(lkg_ctx* ctx) {
   return guarded([&] {
@@ -265,6 +265,7 @@ lkg_status lkg_ctx_trim(lkg_ctx* ctx) {
     ctx->gather.release();
     ctx->hostio.release();
     ctx->xt.release();
+    ctx->ksp.release();
   });
 }
 
@@ -684,7 +685,7 @@ struct lkg_graph {
   // The graph's own hidden-activation and transposed-input buffers: the replayed kernels (and the
   // XT tensor map baked into their parameters) keep pointing at these, so later forwards on the
   // same context may grow or free the context's buffers freely.
-  lkg::DBuf scratch[2], xt;
+  lkg::DBuf scratch[2], xt, ksp;
 };
 
 // Swaps the graph's buffers into the context for the eager pass and the capture, and back out.
@@ -697,6 +698,7 @@ struct GraphBuffers {
     ctx->scratch[0].swap(G->scratch[0]);
     ctx->scratch[1].swap(G->scratch[1]);
     ctx->xt.swap(G->xt);
+    ctx->ksp.swap(G->ksp);
   }
 };
 

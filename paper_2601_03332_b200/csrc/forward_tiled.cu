@@ -83,6 +83,14 @@ struct TiledArgs {
   lkg::CoordConst cc;        // coordinate constants (coords.cuh)
   int64_t n_items, n_rt;
   uint32_t rt_group;    // row tiles per item group (item_coords)
+  // Input split (split-K) of f64-accumulating layers: an item covers n_ihs = n_ih / ksplit
+  // consecutive input tiles of its (row tile, j-block); ksplit > 1 when the layer has too few items to
+  // fill the SMs evenly (a configs[4] column shard on 8 GPUs: 512 items on 148 SMs = 3.46 waves).
+  // A split writes its f64 sums to Ypart[ks][rows][m]; ksplit_reduce_kernel adds the planes in f64, in
+  // split order, and rounds once — the unsplit result up to f64 reassociation (1e-16 relative).
+  int32_t ksplit, n_ihs;
+  double* Ypart;
+  uint32_t* rowflags;   // ksplit > 1: one bit per row, set by the first split that saw it out of range
   int32_t lgL;          // REC: log2(L)
   float4 ktab[kMaxKT];  // {T_k, (L-1)/(T_k+1 - T_k), T_k+1, 0}
   // fused next layer (FUSE): a small-out_dim layer evaluated in the epilogue from the 16 hidden
@@ -153,17 +161,27 @@ __host__ __device__ __forceinline__ int pair_off(int il, int j, int next) {
 // tile in L2). Otherwise groups of a.rt_group row tiles sweep all j-blocks with the row tile
 // fastest: the group's x blocks stay in L2 across j-blocks and each tile is read once per group
 // (C4: DRAM traffic per layer 17 GB -> ~5 GB).
-__device__ __forceinline__ void item_coords(const TiledArgs& a, bool gc, uint32_t u, uint32_t& rt, int& jb) {
-  const uint32_t n_rt = (uint32_t)a.n_rt, n_jb = (uint32_t)a.n_jb, rg = a.rt_group;
+__device__ __forceinline__ void item_coords(const TiledArgs& a, bool gc, uint32_t u, uint32_t& rt, int& jb,
+                                            int& ks) {
+  const uint32_t n_rt = (uint32_t)a.n_rt, rg = a.rt_group, S = (uint32_t)a.ksplit;
+  const uint32_t n_js = (uint32_t)a.n_jb * S;  // (j-block, input split) pairs, split fastest
+  uint32_t js;
   if (gc) {
     rt = u % n_rt;
-    jb = (int)(u / n_rt);
-    return;
+    js = u / n_rt;
+  } else {
+    const uint32_t per = rg * n_js, g = u / per, base = g * rg;
+    const uint32_t gsz = n_rt - base < rg ? n_rt - base : rg, ul = u - g * per;
+    rt = base + ul % gsz;
+    js = ul / gsz;
   }
-  const uint32_t per = rg * n_jb, g = u / per, base = g * rg;
-  const uint32_t gsz = n_rt - base < rg ? n_rt - base : rg, ul = u - g * per;
-  rt = base + ul % gsz;
-  jb = (int)(ul / gsz);
+  if (S == 1) {
+    jb = (int)js;
+    ks = 0;
+  } else {
+    jb = (int)(js / S);
+    ks = (int)(js - (uint32_t)jb * S);
+  }
 }
 
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1, bool GC = false,
@@ -252,13 +270,13 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   }
   const int64_t n_local = bal ? (r_hi - r_lo + TILE_ROWS - 1) / TILE_ROWS
                               : (a.n_items > blockIdx.x ? (a.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0);
-  const int64_t n_stages = n_local * a.n_ih;
+  const int64_t n_stages = n_local * a.n_ihs;
   auto issue = [&](int64_t g, int st) {  // stage g into buffer st = g mod NS
-    const uint32_t gs = (uint32_t)g, item = blockIdx.x + (gs / (uint32_t)a.n_ih) * gridDim.x;
+    const uint32_t gs = (uint32_t)g, item = blockIdx.x + (gs / (uint32_t)a.n_ihs) * gridDim.x;
     uint32_t rt_ = 0;
-    int jb = 0;  // balanced rows: the only j-block (local item numbers are not global item ids)
-    if (!bal) item_coords(a, GC, item, rt_, jb);
-    const int ih = (int)(gs % (uint32_t)a.n_ih);
+    int jb = 0, ks_ = 0;  // balanced rows: the only j-block (local item numbers are not global item ids)
+    if (!bal) item_coords(a, GC, item, rt_, jb, ks_);
+    const int ih = ks_ * a.n_ihs + (int)(gs % (uint32_t)a.n_ihs);
     const uint8_t* src = a.tiles + ((int64_t)jb * a.n_ih + ih) * tb + so;
     uint8_t* dst = stage + st * sb;
     mbar_expect_tx(&full[st], (uint32_t)sb);
@@ -288,9 +306,16 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
     if (bal) return r_lo + li_ * TILE_ROWS + warp * ROWS_W;
     const uint32_t item_ = (uint32_t)(blockIdx.x + li_ * gridDim.x);
     uint32_t rt_;
-    int jb_;
-    item_coords(a, GC, item_, rt_, jb_);
+    int jb_, ks_;
+    item_coords(a, GC, item_, rt_, jb_, ks_);
     return (int64_t)rt_ * (W * ROWS_W) + warp * ROWS_W;
+  };
+  auto ih0_of = [&](int64_t li_) -> int {  // first input tile of local item li (its input split)
+    if (bal || a.ksplit == 1) return 0;
+    uint32_t rt_;
+    int jb_, ks_;
+    item_coords(a, GC, (uint32_t)(blockIdx.x + li_ * gridDim.x), rt_, jb_, ks_);
+    return ks_ * a.n_ihs;
   };
   uint32_t xphase = 0;
   auto stage_x = [&](int64_t r0_, int ih_, int buf) {
@@ -342,16 +367,17 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  if (n_local > 0) stage_x(row0_of(0), 0, 0);
+  if (n_local > 0) stage_x(row0_of(0), ih0_of(0), 0);
   int xbuf = 0;
 
   for (int64_t li = 0; li < n_local; li++) {
     const uint32_t item = (uint32_t)(blockIdx.x + li * gridDim.x);
     uint32_t rt32 = 0;
-    int jb = 0;
-    if (!bal) item_coords(a, GC, item, rt32, jb);
+    int jb = 0, ks = 0;
+    if (!bal) item_coords(a, GC, item, rt32, jb, ks);
     const int64_t rt = rt32;
     const int64_t row0_next = li + 1 < n_local ? row0_of(li + 1) : 0;
+    const int ih0 = ks * a.n_ihs, ih0_next = li + 1 < n_local ? ih0_of(li + 1) : 0;
     const int cnt = jb == 0;  // OOB statistics are counted once per row (j-block 0)
     const int64_t row0 = bal ? row0_of(li) : rt * TILE_ROWS + warp * ROWS_W;
     const int64_t rows_left = r_hi - row0;  // rows of this warp: [0, min(ROWS_W, rows_left))
@@ -369,7 +395,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       }
     }
 
-    for (int ih = 0; ih < a.n_ih; ih++, g++) {
+    for (int ih = ih0; ih < ih0 + a.n_ihs; ih++, g++) {
       // this tile's x block has landed (this lane's copies, then the warp's); prefetch the next
       if constexpr (XT) {
         mbar_wait(&xbar[warp], xphase);
@@ -380,10 +406,10 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       __syncwarp();
       const float* xs = xsw + (XB == 2 ? xbuf * G * XS * XW : 0);
       if constexpr (XB == 2) {
-        if (ih + 1 < a.n_ih)
+        if (ih + 1 < ih0 + a.n_ihs)
           stage_x(row0, ih + 1, xbuf ^ 1);
         else if (li + 1 < n_local)
-          stage_x(row0_next, 0, xbuf ^ 1);
+          stage_x(row0_next, ih0_next, xbuf ^ 1);
         xbuf ^= 1;
       }
       const int st = (int)((uint32_t)g % NS);  // constant divisor: multiply-shift
@@ -585,7 +611,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           }
         }
       }
-      if (F64 && ((ih + 1) % kFlushBlocks == 0 || ih + 1 == a.n_ih)) {
+      if (F64 && ((ih + 1) % kFlushBlocks == 0 || ih + 1 == ih0 + a.n_ihs)) {
         // fp32 tile partials into the f64 accumulators in TMEM (lo/hi word pairs)
 #pragma unroll
         for (int r = 0; r < R; r++) {
@@ -606,10 +632,10 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       }
       if constexpr (XB == 1) {
         __syncwarp();  // one x buffer: the next block is staged once every lane is done with this one
-        if (ih + 1 < a.n_ih)
+        if (ih + 1 < ih0 + a.n_ihs)
           stage_x(row0, ih + 1, 0);
         else if (li + 1 < n_local)
-          stage_x(row0_next, 0, 0);
+          stage_x(row0_next, ih0_next, 0);
       }
       // Stage release without a CTA barrier: the last warp done with this buffer refills it, so
       // warps drift up to NS-1 stages apart instead of re-aligning at every tile.
@@ -634,6 +660,14 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
       if (F64) {  // warp-collective TMEM read: every lane, before the row bound
         uint32_t w[32];
         lkg::tmem_ld32(tm_warp + 32 * r, w);
+        if (a.ksplit > 1) {  // input split: this split's f64 sums go to its plane (ksplit_reduce_kernel)
+          if (lane + 32 * r < rows_left) {
+            double* pr = a.Ypart + ((int64_t)ks * a.rows + row) * a.m + j0;
+#pragma unroll
+            for (int q = 0; q < 16; q++)
+              if (j0 + q < a.m) pr[q] = __hiloint2double((int)w[2 * q + 1], (int)w[2 * q]);
+          }
+        }
 #pragma unroll
         for (int q = 0; q < 16; q++) out[q] = (float)__hiloint2double((int)w[2 * q + 1], (int)w[2 * q]);
       } else {
@@ -696,7 +730,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
           y2r[0] = y2.x;
           if (a.m2 > 1) y2r[1] = y2.y;
           oob2_rows += (uint32_t)r_oob2;
-        } else {
+        } else if (a.ksplit == 1) {
           float* yr = a.Y + row * a.m + j0;
           LKG_DCHECK(row >= 0 && row < a.rows && j0 < a.m, "output coordinate out of range");
           if (j0 + 16 <= a.m && (a.m & 3) == 0) {
@@ -709,7 +743,15 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
               if (j0 + q < a.m) yr[q] = out[q];
           }
         }
-        oob_rows += (uint32_t)(cnt & (row_oob >> r));
+        if (a.ksplit > 1) {
+          // a row's inputs are spread over the splits: the first split to flag the row counts it
+          if (cnt & (row_oob >> r)) {
+            const uint32_t bit = 1u << (row & 31);
+            oob_rows += (uint32_t)((atomicOr(a.rowflags + (row >> 5), bit) & bit) == 0u);
+          }
+        } else {
+          oob_rows += (uint32_t)(cnt & (row_oob >> r));
+        }
       }
     }
   }
@@ -1590,6 +1632,47 @@ static void encode_x_map(CUtensorMap* map, const float* Xt, int64_t rows, int d,
     throw Error{LKG_ERR_CUDA, "cuTensorMapEncodeTiled failed"};
 }
 
+// Y = the f64 sum of the input splits' planes, in split order, rounded once to f32.
+__global__ void ksplit_reduce_kernel(const double* __restrict__ part, int64_t n, int32_t S, float* __restrict__ Y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double v = part[i];
+  for (int s = 1; s < S; s++) v += part[(int64_t)s * n + i];
+  Y[i] = (float)v;
+}
+
+// Input splits per (row tile, j-block) so that the items fill the SMs evenly: the persistent grid
+// runs ceil(items / SMs) waves, and a layer with few items (a configs[4] column shard on 8 GPUs:
+// 512 items = 3.46 waves on 148 SMs, i.e. 4) loses the unused part of the last one. Splitting the
+// inputs S ways makes S times as many items of 1/S the length. LKG_KSPLIT=n forces n (1 = off).
+static int choose_ksplit(int64_t items, int sms, int n_ih, int64_t rows, int m) {
+  static const char* env = getenv("LKG_KSPLIT");
+  // at least 8 tiles per item; the f64 planes bounded at 1 GB
+  auto ok = [&](int S) {
+    return S == 1 || (S > 1 && n_ih % S == 0 && n_ih / S >= 8 && rows * (int64_t)m * S <= (128ll << 20));
+  };
+  if (env) {
+    const int S = atoi(env);
+    return ok(S) ? S : 1;
+  }
+  auto eff = [&](int S) {
+    const int64_t I = items * S, waves = (I + sms - 1) / sms;
+    return (double)I / (double)(waves * sms);
+  };
+  int best = 1;
+  double be = eff(1);
+  if (be >= 0.93) return 1;
+  for (int S = 2; S <= 8; S *= 2) {
+    if (!ok(S)) break;
+    const double e = eff(S) - 0.01 * S;  // (each split adds an epilogue and a plane of partials)
+    if (e > be + 0.03) {
+      best = S;
+      be = e;
+    }
+  }
+  return best;
+}
+
 void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk, float* Y,
                           int slot, const lkg_layer* L2, float* Y2) {
   const TileGeom& gm = L->geom;
@@ -1626,6 +1709,24 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   // spreads even a small batch over every SM (>= 64 rows per CTA): a 4096-row configs[1] batch took
   // the time of one whole 1024-row item on each of 4 CTAs.
   const bool bal_mode = !f64 && gm.n_jb == 1 && !gm.codes_global;
+  a.ksplit = (!f64 || L2 || rows <= 0) ? 1 : choose_ksplit(a.n_items, sm_count(ctx->device), gm.n_ih, rows, a.m);
+  a.n_ihs = gm.n_ih / a.ksplit;
+  a.n_items *= a.ksplit;
+  if (a.ksplit > 1) {  // f64 planes of partial sums, then the row flags of the OOB row count (zeroed per launch)
+    const size_t plane = (size_t)rows * a.m * sizeof(double), flags = (size_t)((rows + 31) / 32) * 4;
+    const size_t need = a.ksplit * plane + flags;
+    if (ctx->ksp.bytes < need) ctx->ksp.alloc(need);
+    a.Ypart = ctx->ksp.as<double>();
+    a.rowflags = reinterpret_cast<uint32_t*>(ctx->ksp.as<uint8_t>() + a.ksplit * plane);
+    LKG_CUDA(cudaMemsetAsync(a.rowflags, 0, flags, ctx->stream));
+  }
+  auto reduce_splits = [&] {
+    if (a.ksplit <= 1) return;
+    const int64_t n = rows * (int64_t)a.m;
+    ksplit_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(a.Ypart, n, a.ksplit, Y);
+    LKG_CUDA(cudaGetLastError());
+    ctx->launches++;
+  };
   const int grid = bal_mode ? (int)std::max<int64_t>(1, std::min<int64_t>((rows + 63) / 64, sm_count(ctx->device)))
                             : (int)std::min<int64_t>(a.n_items, sm_count(ctx->device));
   {  // row tiles per item group (item_coords). Measured on configs[3] layer 1 (1M rows): 4/8/16/32
@@ -1699,6 +1800,7 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
     }
     LKG_CUDA(cudaGetLastError());
     ctx->launches++;
+    reduce_splits();
     return;
   }
   if (gm.codes_global) {
@@ -1715,6 +1817,7 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
     }
     LKG_CUDA(cudaGetLastError());
     ctx->launches++;
+    reduce_splits();
     return;
   }
   if (L2) {  // fused chain step: this layer + the small next layer in one launch
@@ -1764,6 +1867,7 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   }
   LKG_CUDA(cudaGetLastError());
   ctx->launches++;
+  reduce_splits();
 }
 
 }  // namespace lkg

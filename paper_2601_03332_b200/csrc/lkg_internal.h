@@ -130,6 +130,7 @@ struct lkg_ctx {
   lkg::DBuf gather;      // sharded chain: all-gathered hidden activations
   lkg::DBuf hostio;      // device staging for lkg_model_forward_host
   lkg::DBuf xt;          // transposed layer input of the XT table walk (forward_tiled.cu)
+  lkg::DBuf ksp;         // input-split partial outputs + row flags (forward_tiled.cu, ksplit)
   void* pin = nullptr;                 // pinned host staging of the f64 host entry (grows)
   size_t pin_bytes = 0;
   cudaStream_t copy_stream = nullptr;  // H2D of the next chunk overlaps the chain on `stream`

@@ -254,6 +254,46 @@ def test_chain_c1(lk, oracle):
     assert np.array_equal(r.Y, Y2)
 
 
+def test_input_split_items(lk, oracle, tmp_path):
+    """f64-accumulating layers with too few (row tile, j-block) items to fill the SMs split each
+    item's inputs S ways (split-K): a split writes its f64 sums to a plane, a reduce kernel adds the
+    planes in f64 in split order and rounds once. Forced S = 2, 4, 8 (LKG_KSPLIT) against S = 1:
+    identical OobStats (OOB rows counted once through row flags) and the same outputs up to f64
+    reassociation before the one f32 rounding (at most a stray last-bit difference); repeat launches
+    bit-identical; the automatic choice against the reference."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = (
+        "import sys, numpy as np, torch; sys.path[:0] = [%r, %r]\n"
+        "import paper_2601_03332_b200 as lk\n"
+        "for t, (d, m, rows, s) in enumerate(((1024, 512, 2048, 0), (256, 64, 1000, 1), (512, 48, 3000, 0))):\n"
+        "    a = lk.compile_layer(lk.gen_layer(40 + t, d, m, 8), lk.QuantConfig(64, lk.Scheme(s), lk.Dtype(s)),"
+        " lk.OobConfig(lk.BoundaryMode.Closed, lk.OobPolicy(s)))\n"
+        "    X = torch.from_numpy(np.random.default_rng(t).uniform(-1.3, 1.3, (rows, d)).astype(np.float32)).cuda()\n"
+        "    Y, st = lk.lut_layer_forward_batch(a, X)\n"
+        "    Y2, st2 = lk.lut_layer_forward_batch(a, X)\n"
+        "    assert torch.equal(Y, Y2) and st.n_oob_samples == st2.n_oob_samples\n"
+        "    np.save(%r + '/y%%d.npy' %% t, Y.cpu().numpy())\n"
+        "    np.save(%r + '/s%%d.npy' %% t, np.array([st.n_oob_samples, st.n_oob_inputs, st.n_samples, st.n_inputs]))\n"
+    ) % (os.path.dirname(here), here, str(tmp_path), str(tmp_path))
+    outs = {}
+    for S in ("1", "2", "4", "8"):
+        subprocess.run([sys.executable, "-c", code], env=dict(os.environ, LKG_KSPLIT=S), check=True)
+        outs[S] = [(np.load(tmp_path / f"y{t}.npy"), np.load(tmp_path / f"s{t}.npy")) for t in range(3)]
+    for S in ("2", "4", "8"):
+        for (y1, s1), (yS, sS) in zip(outs["1"], outs[S]):
+            assert np.array_equal(s1, sS)
+            diff = y1 != yS
+            assert np.count_nonzero(diff) <= 2 and np.all(np.abs(y1 - yS) <= 1.2e-7 * np.maximum(1.0, np.abs(y1)))
+    # the automatic choice (64 items on 148 SMs: split) against the reference
+    so = oracle.gen_layer(40, 1024, 512, 8)
+    art = oracle.compile_layer(so, 64, 0, 1, 0, 1, 0)
+    X = np.random.default_rng(0).uniform(-1.3, 1.3, (2048, 1024)).astype(np.float32)
+    _layer_parity(lk, oracle, art, X, "split-K 1024->512")
+
+
 def test_workspace_report_and_trim(lk):
     """The context reports the device workspace it keeps between calls (hidden activations, the
     coordinate-record buffer of the wide-layer walk) and frees it on request; it regrows on demand."""
