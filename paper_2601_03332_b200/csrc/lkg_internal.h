@@ -76,6 +76,10 @@ struct TileGeom {
   // standard lines, pairs built with one PRMT per 2 outputs. P is stored pre-scaled by 2^-15.
   int32_t idp = 0;
   double idp_rss = 0.0;       // statistical bound of the 2^-16 weight-rounding error (build_tiles)
+  // fp32-accumulation error estimate of the layer (build_tiles) and whether it therefore takes the
+  // f64 accumulators although d <= 256
+  double acc32_err = 0.0;
+  int32_t acc64 = 0;
 };
 
 }  // namespace lkg
@@ -112,6 +116,7 @@ struct lkg_spec {
   lkg::DBuf spline_tiles;  // spline_tiled.cu layout (uniform cubic grids), built lazily
   lkg::DBuf tc_b;          // spline_tc.cu: the coefficient matrix in UMMA blocks (hi/lo tf32), lazily
   int32_t tc_n_ch = 0;
+  double fast_err = -1.0;  // rounding estimate of the fast spline kernels (spline.cu), computed once
   int64_t sp_tile_bytes = 0;
   int32_t sp_n_ih = 0, sp_n_jb = 0;
 };

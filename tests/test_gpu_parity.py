@@ -705,7 +705,8 @@ def test_element_primitives_spline_and_quantize(lk, oracle):
 
 
 # ------------------------------------------------------------------ randomized shapes
-@pytest.mark.parametrize("seed", range(80))
+# (LKG_FUZZ_SEEDS widens the campaign: profiles/r02g/fuzz_1000.log is a 1000-seed run)
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("LKG_FUZZ_SEEDS", "80"))))
 def test_fuzz_compile_and_forward(lk, oracle, seed):
     """Random layer shapes, grids and contracts (d, m off the 8/16 tile multiples; K up to 40;
     L from 2 to 160; uneven knots; phi and spline_component; f16 params; all boundary/OOB
@@ -738,7 +739,7 @@ def test_fuzz_compile_and_forward(lk, oracle, seed):
     _layer_parity(lk, oracle, ao, X, f"fuzz {seed}: d{d} m{m} K{K} deg{deg} L{L} s{scheme} vr{vr} pd{pd} bm{bm} op{op}")
 
 
-@pytest.mark.parametrize("seed", range(30))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("LKG_FUZZ_SPLINE_SEEDS", "30"))))
 def test_fuzz_spline_forward(lk, oracle, seed):
     """Random spline layers through layer_forward_batch (tiled kernel on uniform cubic grids,
     generic kernel otherwise) against the reference's spline forward."""
