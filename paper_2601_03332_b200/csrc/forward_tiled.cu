@@ -185,13 +185,14 @@ __device__ __forceinline__ void item_coords(const TiledArgs& a, bool gc, uint32_
 }
 
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE, int MINB = 1, bool GC = false,
-          bool BAL = false, int XB = 1, bool XT = false, int IDPM = 0, bool REC = false>
+          bool BAL = false, int XB = 1, bool XT = false, int IDPM = 0, bool REC = false, int NSX = 0>
 __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant__ TiledArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   // Two stage buffers, a compile-time count: NS as a runtime value turned every per-tile
   // g mod NS into a 64-bit division (configs[1] layer 0: 0.567 -> 0.534 ms once removed). Three
   // (LKG_NS=3, the most that fits next to the x tiles) measured 8.5% slower on configs[1].
-  constexpr int NS = LKG_NS;
+  // (NSX: the small-batch variant runs 4 stages — its chain of tile loads is latency-bound)
+  constexpr int NS = NSX ? NSX : LKG_NS;
   constexpr int ROWS_W = 32 * R;        // rows per warp
   // row stride of the transposed x tile: padded for the 4-byte cp.async writes, or exactly the TMA
   // box (XT; the rotated reads xs[il][lane + 32r] are conflict-free either way)
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(W * 32, MINB) fwd_tiled(const __grid_constant_
   int64_t r_lo = 0, r_hi = a.rows;
   if (bal) {
     auto split = [&](int64_t b) -> int64_t {
-      return b >= (int64_t)gridDim.x ? a.rows : (a.rows * b / (int64_t)gridDim.x) / 64 * 64;
+      return b >= (int64_t)gridDim.x ? a.rows : (a.rows * b / (int64_t)gridDim.x) / ROWS_W * ROWS_W;
     };
     r_lo = split(blockIdx.x);
     r_hi = split((int64_t)blockIdx.x + 1);
@@ -836,13 +837,28 @@ __global__ void __launch_bounds__(1024) fwd_small(const __grid_constant__ SmallA
   float4* ktab = reinterpret_cast<float4*>(smem + ((a.lut_bytes + 15) & ~15));
   float2* kf = reinterpret_cast<float2*>(ktab + kMaxKT);  // compact {T_k, (L-1)/h_k} (coords.cuh)
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int o = tid * 16; o < a.lut_bytes; o += blockDim.x * 16)
-    *reinterpret_cast<uint4*>(lut + o) = __ldg(reinterpret_cast<const uint4*>(a.lut + o));
+  // the table arrives by TMA bulk copies issued by one thread (small batches run small blocks, where
+  // a per-thread copy loop is a chain of L2 round trips); odd sizes take the loop
+  __shared__ __align__(8) uint64_t tbar;
+  const bool bulk = (a.lut_bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(a.lut) & 15) == 0;
+  if (bulk) {
+    if (tid == 0) {
+      mbar_init(&tbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&tbar, (uint32_t)a.lut_bytes);
+      for (int32_t o = 0; o < a.lut_bytes; o += 32768)
+        bulk_g2s(lut + o, a.lut + o, (uint32_t)(a.lut_bytes - o < 32768 ? a.lut_bytes - o : 32768), &tbar);
+    }
+  } else {
+    for (int o = tid * 16; o < a.lut_bytes; o += blockDim.x * 16)
+      *reinterpret_cast<uint4*>(lut + o) = __ldg(reinterpret_cast<const uint4*>(a.lut + o));
+  }
   for (int k = tid; k < a.cc.K; k += blockDim.x) {
     ktab[k] = a.ktab[k];
     kf[k] = make_float2(a.ktab[k].x, a.ktab[k].y);
   }
   __syncthreads();
+  if (bulk) mbar_wait(&tbar, 0);
   const float lo = a.cc.lo;
   const int K = a.cc.K, L = a.cc.L, d = a.d, MP = VT ? MPT : a.MP;
   const int64_t x_rs = a.x_blk > 0 ? a.x_blk : d;
@@ -1167,9 +1183,9 @@ __global__ void idp_bound_kernel(const uint8_t* q, const float* scale, const flo
 }
 
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1, bool GC = false,
-          bool BAL = false, int XB = 1, bool XT = false, int IDPM = 0, bool REC = false>
+          bool BAL = false, int XB = 1, bool XT = false, int IDPM = 0, bool REC = false, int NSX = 0>
 void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
-  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, IDPM, REC>;
+  auto kern = fwd_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, IDPM, REC, NSX>;
   static bool attr = false;
   if (!attr) {
     LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -1183,8 +1199,15 @@ void launch_tiled(cudaStream_t st, const TiledArgs& a, size_t smem, int grid) {
 // The layer's table walk (TileGeom::idp) as a runtime choice over the compiled variants; pair lines
 // are never used with codes in global memory.
 template <int R, int W, bool ASYM, bool SR, bool ZS, bool F64, bool FUSE = false, int MINB = 1, bool GC = false,
-          bool BAL = false, int XB = 1, bool XT = false>
+          bool BAL = false, int XB = 1, bool XT = false, int NSX = 0>
 void launch_idp(int idp, cudaStream_t st, const TiledArgs& a, size_t smem, int grid, bool rec = false) {
+  if constexpr (NSX != 0) {  // the small-batch variant: standard lines only (integer or fp32 lerp)
+    if (idp == 2)
+      launch_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, 2, false, NSX>(st, a, smem, grid);
+    else
+      launch_tiled<R, W, ASYM, SR, ZS, F64, FUSE, MINB, GC, BAL, XB, XT, 0, false, NSX>(st, a, smem, grid);
+    return;
+  }
   if constexpr (XT) {
     if (rec) {  // coordinate records (coord_pass_kernel) over the standard lines / the GC pair entries
       if constexpr (GC) {
@@ -1511,14 +1534,14 @@ static int sm_count(int dev) {
 }
 
 template <bool ASYM, bool SR, bool ZS, bool VT, int MPT, bool VP = false>
-static void launch_small_t(cudaStream_t st, const SmallArgs& a, size_t smem, int grid) {
+static void launch_small_t(cudaStream_t st, const SmallArgs& a, size_t smem, int grid, int block) {
   auto kern = fwd_small<ASYM, SR, ZS, VT, MPT, VP>;
   static bool attr = false;
   if (!attr) {
-    LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    LKG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 224 * 1024));  // (+ the barrier)
     attr = true;
   }
-  kern<<<grid, 1024, smem, st>>>(a);
+  kern<<<grid, block, smem, st>>>(a);
 }
 
 static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* X, int64_t rows, int32_t x_blk,
@@ -1539,8 +1562,11 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
   a.m = L->col1 - L->col0;
   a.counters = ctx->counters.as<unsigned long long>() + 4 * slot;
   fill_coord_const(L, a.cc, a.ktab);
-  // one resident block per SM (1024 threads x ~47 registers) and one equal row range per block
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 1023) / 1024, sm_count(ctx->device)));
+  // one resident block per SM (1024 threads x ~47 registers) and one equal row range per block; a
+  // small batch takes smaller blocks so that it still spreads over the SMs (a 4096-row batch ran on 4)
+  int block = 1024;
+  while (block > 128 && rows < (int64_t)sm_count(ctx->device) * block) block >>= 1;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + block - 1) / block, sm_count(ctx->device)));
   const size_t smem = ((gm.tile_bytes + 15) & ~15) + kMaxKT * 16 + kMaxKT * 8;
   const bool asym = L->scheme == LKG_SCHEME_ASYMMETRIC, sr = L->value_repr == LKG_REPR_SPLINE_COMPONENT;
   const bool zs = L->oob_policy == LKG_OOB_ZERO_SPLINE;
@@ -1551,7 +1577,7 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
 #define CASE(S)                                                                                                  \
   case S:                                                                                                        \
     launch_small_t<false, (S >> 1) & 1, S & 1, true, 1 << ((S >> 2) & 3), ((S >> 4) & 1) != 0>(ctx->stream, a, \
-                                                                                               smem, grid);     \
+                                                                                        smem, grid, block);     \
     break;
       CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
       CASE(8) CASE(9) CASE(10) CASE(11) CASE(12) CASE(13) CASE(14) CASE(15)
@@ -1562,7 +1588,7 @@ static void launch_forward_small(lkg_ctx* ctx, const lkg_layer* L, const float* 
   } else {
     switch ((asym << 2) | sz) {
 #define CASE(S) \
-  case S: launch_small_t<(S >> 2) & 1, (S >> 1) & 1, S & 1, false, 8>(ctx->stream, a, smem, grid); break;
+  case S: launch_small_t<(S >> 2) & 1, (S >> 1) & 1, S & 1, false, 8>(ctx->stream, a, smem, grid, block); break;
       CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
 #undef CASE
     }
@@ -1909,6 +1935,29 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
     return;
   }
   const bool bal = bal_mode;
+  // Small batches of a one-j-block layer (serving): with 2 rows per lane a 4096-row configs[1] batch
+  // is 64 single-warp CTAs walking 10 tiles each, latency-bound (36 us). One row per lane (R = 1)
+  // doubles the warps and halves each one's work per tile; same lane and input order per row, so the
+  // same bits (test_balanced_rows_small_batches_bit_identical). LKG_R1=0 disables.
+  static const char* r1_env = getenv("LKG_R1");
+  const bool r1 = bal && !(r1_env && r1_env[0] == '0') && rows <= (int64_t)64 * sm_count(ctx->device) &&
+                  gm.idp != 1 && tiled_smem(L, W, 1, 4) <= 227 * 1024;  // (4 stage buffers: see NSX)
+  if (r1) {
+    smem = tiled_smem(L, W, 1, 4);
+    const int grid1 = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 31) / 32, sm_count(ctx->device)));
+    switch (sel) {
+#define CASE(S)                                                                                                  \
+  case S:                                                                                                        \
+    launch_idp<1, kW, (S >> 2) & 1, (S >> 1) & 1, S & 1, false, false, 1, false, true, 1, false, 4>(           \
+        gm.idp, ctx->stream, a, smem, grid1);                                                                    \
+    break;
+      CASE(0) CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7)
+#undef CASE
+    }
+    LKG_CUDA(cudaGetLastError());
+    ctx->launches++;
+    return;
+  }
   // two x buffers only for the int8 one-j-block layers (see fwd_tiled's XB), where they fit
   const bool xb2 = bal && !asym && tiled_smem(L, W, R, LKG_NS, 2) <= 227 * 1024;
   if (xb2) smem = tiled_smem(L, W, R, LKG_NS, 2);
