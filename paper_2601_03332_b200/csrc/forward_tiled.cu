@@ -777,15 +777,24 @@ bool can_fuse(const lkg_layer* L1, const lkg_layer* L2) {
 // X [rows][d] -> Xt [d][rows] (32x32 tiles through shared memory, both sides coalesced), and the
 // base-branch activations St = silu(zs ? x : clamp(x, t_0, hi_clip)) in the same layout (f64, one
 // rounding to f32: each element once, instead of once per j-block inside the table walk).
-__global__ void transpose_kernel(const float* __restrict__ X, int64_t rows, int32_t d, float* __restrict__ Xt,
-                                 float* __restrict__ St, float lo, float hi_clip, int zs, int exact) {
+// (x_blk > 0: X is in the rank-major all-gather layout, element (r, i) at
+// X[(i / x_blk) * rows * x_blk + r * x_blk + i % x_blk])
+__device__ __forceinline__ int64_t x_index(int64_t r, int c, int64_t rows, int32_t d, int32_t x_blk) {
+  if (x_blk <= 0) return r * d + c;
+  const int b = c / x_blk;
+  return (int64_t)b * rows * x_blk + r * x_blk + (c - b * x_blk);
+}
+
+__global__ void transpose_kernel(const float* __restrict__ X, int64_t rows, int32_t d, int32_t x_blk,
+                                 float* __restrict__ Xt, float* __restrict__ St, float lo, float hi_clip, int zs,
+                                 int exact) {
   __shared__ float t[32][33];
   const int64_t r0 = (int64_t)blockIdx.x * 32;
   const int c0 = blockIdx.y * 32;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int64_t r = r0 + k;
     const int c = c0 + threadIdx.x;
-    if (r < rows && c < d) t[k][threadIdx.x] = X[r * d + c];
+    if (r < rows && c < d) t[k][threadIdx.x] = X[x_index(r, c, rows, d, x_blk)];
   }
   __syncthreads();
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -814,8 +823,8 @@ struct CoordPassArgs {
 };
 
 __global__ void coord_pass_kernel(const __grid_constant__ CoordPassArgs c, const float* __restrict__ X, int64_t rows,
-                                  int32_t d, int64_t ld, uint32_t* __restrict__ Rt, float* __restrict__ St, int zs,
-                                  int exact, unsigned long long* nonfinite) {
+                                  int32_t d, int32_t x_blk, int64_t ld, uint32_t* __restrict__ Rt,
+                                  float* __restrict__ St, int zs, int exact, unsigned long long* nonfinite) {
   __shared__ float t[32][33];
   __shared__ float4 ktab[kMaxKT];
   __shared__ float2 kf[kMaxKT];
@@ -829,7 +838,7 @@ __global__ void coord_pass_kernel(const __grid_constant__ CoordPassArgs c, const
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int64_t r = r0 + k;
     const int col = c0 + threadIdx.x;
-    if (r < rows && col < d) t[k][threadIdx.x] = X[r * d + col];
+    if (r < rows && col < d) t[k][threadIdx.x] = X[x_index(r, col, rows, d, x_blk)];
   }
   __syncthreads();
   bool bad = false;
@@ -998,10 +1007,10 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
   static const char* rec_env = getenv("LKG_REC");
   const int Ls = L->L;
   const bool rec = !(rec_env && rec_env[0] == '0') && (gm.idp == 2 || gm.idp == 3) && (Ls & (Ls - 1)) == 0 && L->K * Ls <= 8192 &&
-                   !L2 && x_blk <= 0 && gm.n_jb >= 4 && rows > 0 && rows < (1ll << 31) &&
+                   !L2 && gm.n_jb >= 4 && rows > 0 && rows < (1ll << 31) &&
                    (!gm.codes_global || xt_gc_ok);
   const bool xt = rec || (!(xt_env && xt_env[0] == '0') && (!gm.codes_global || xt_gc_ok) && !L2 && gm.n_jb >= 16 &&
-                          x_blk <= 0 && rows % row_tile == 0 && L->in_dim % G == 0 && rows < (1ll << 31));
+                          rows % row_tile == 0 && L->in_dim % G == 0 && rows < (1ll << 31));
   if (xt) {
     const int64_t ld = (rows + 3) / 4 * 4;  // 16-byte tensor-map strides
     const size_t xt_elems = (size_t)ld * L->in_dim;
@@ -1013,19 +1022,20 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
       CoordPassArgs ca{};
       ca.cc = a.cc;
       for (int k = 0; k < a.cc.K; k++) ca.ktab[k] = a.ktab[k];
-      coord_pass_kernel<<<tgrid, dim3(32, 8), 0, ctx->stream>>>(ca, X, rows, L->in_dim, ld,
+      coord_pass_kernel<<<tgrid, dim3(32, 8), 0, ctx->stream>>>(ca, X, rows, L->in_dim, x_blk, ld,
                                                                reinterpret_cast<uint32_t*>(Xt), St, zs, f64,
                                                                a.counters + 2);
       a.lgL = __builtin_ctz((unsigned)Ls);
     } else {
-      transpose_kernel<<<tgrid, dim3(32, 8), 0, ctx->stream>>>(X, rows, L->in_dim, Xt, St, a.cc.lo, a.cc.hi_clip,
-                                                               zs, f64);
+      transpose_kernel<<<tgrid, dim3(32, 8), 0, ctx->stream>>>(X, rows, L->in_dim, x_blk, Xt, St, a.cc.lo,
+                                                               a.cc.hi_clip, zs, f64);
     }
     LKG_CUDA(cudaGetLastError());
     ctx->launches++;
     encode_x_map(&a.xmap, Xt, rows, L->in_dim, 32 * R, G, ld);
     encode_x_map(&a.smap, St, rows, L->in_dim, 32 * R, G, ld);
     a.X = Xt;
+    a.x_blk = 0;  // (the passes read the blocked all-gather layout; the walk reads their [d][rows] output)
     smem += (size_t)W * G * (32 * R) * 4;  // the silu boxes
     tiled::launch_xt(sel, f64, gm.codes_global != 0, gm.idp, ctx->stream, a, smem, grid, rec);
     LKG_CUDA(cudaGetLastError());

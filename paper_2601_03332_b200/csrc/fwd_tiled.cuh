@@ -1,4 +1,4 @@
-// forward_tiled.cu — K2 on sm_100a: shared-memory-staged LUT forward.
+// fwd_tiled.cuh — K2 on sm_100a: the shared-memory-staged LUT forward kernel (table walk) and its launchers.
 //
 // Replaces forward_quant<SR,ZS,I8> (proj/core/src/runtime.cpp:135-223) for artifacts whose
 // per-stage LUT tile fits shared memory. Design:

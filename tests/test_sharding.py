@@ -140,6 +140,26 @@ def test_column_shards_and_blocked_input_gpu(lk, oracle, engine):
 
 
 @pytest.mark.gpu
+def test_blocked_input_into_record_walk_gpu(lk, engine):
+    """Wide layers of a column-sharded chain read the all-gathered activations in rank-major blocks:
+    the coordinate-record / transposed-input passes take that layout directly, so such layers keep
+    the record walk (and its bits) behind an all-gather. A 64 -> 64 layer (4 j-blocks, fp32) from 2
+    blocks of 32 and a 1024 -> 256 layer (16 j-blocks, f64 TMEM) from 4 blocks of 256, both against the
+    row-major call."""
+    import torch
+    from paper_2601_03332_b200.sharding import layer_forward_blocked, rowmajor_to_blocked
+    oob = lk.OobConfig(lk.BoundaryMode.HalfOpen, lk.OobPolicy.ClipX)
+    for spec, rows, world in ((lk.recipe_layer(3, 0), 3001, 2), (lk.gen_layer(9, 1024, 256, 8), 2048, 4)):
+        art = lk.compile_layer(spec, lk.QuantConfig(64), oob, engine=engine)
+        X = np.random.default_rng(rows).uniform(-1.2, 1.2, (rows, spec.in_dim)).astype(np.float32)
+        Yr, st_r = lk.lut_layer_forward_batch(art, torch.from_numpy(X).cuda(), engine=engine)
+        blk = torch.from_numpy(rowmajor_to_blocked(X, world)).cuda()
+        Yb, st_b = layer_forward_blocked(art, blk, spec.in_dim // world, engine)
+        assert torch.equal(Yb, Yr)
+        assert (st_b.n_oob_inputs, st_b.n_oob_samples) == (st_r.n_oob_inputs, st_r.n_oob_samples)
+
+
+@pytest.mark.gpu
 def test_nccl_sharded_chain_one_rank(lk, engine):
     import torch
     from paper_2601_03332_b200.sharding import ColumnShardedChain
