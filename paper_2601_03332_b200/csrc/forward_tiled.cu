@@ -822,10 +822,12 @@ struct CoordPassArgs {
   float4 ktab[kMaxKT];
 };
 
+constexpr int kCoordSub = 8;  // 32-row sub-tiles per coord_pass block (32 columns x 256 rows)
+
 __global__ void coord_pass_kernel(const __grid_constant__ CoordPassArgs c, const float* __restrict__ X, int64_t rows,
                                   int32_t d, int32_t x_blk, int64_t ld, uint32_t* __restrict__ Rt,
                                   float* __restrict__ St, int zs, int exact, unsigned long long* nonfinite) {
-  __shared__ float t[32][33];
+  __shared__ float t[2][32][33];
   __shared__ float4 ktab[kMaxKT];
   __shared__ float2 kf[kMaxKT];
   const int tid = threadIdx.y * 32 + threadIdx.x;
@@ -833,33 +835,42 @@ __global__ void coord_pass_kernel(const __grid_constant__ CoordPassArgs c, const
     ktab[q] = c.ktab[q];
     kf[q] = make_float2(c.ktab[q].x, c.ktab[q].y);
   }
-  const int64_t r0 = (int64_t)blockIdx.x * 32;
+  // a block walks kCoordSub 32x32 sub-tiles down the rows (one barrier each: the tile buffer is
+  // double-buffered), so the table staging and the index set-up serve 32 elements per thread, not 4
   const int c0 = blockIdx.y * 32;
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    const int64_t r = r0 + k;
-    const int col = c0 + threadIdx.x;
-    if (r < rows && col < d) t[k][threadIdx.x] = X[x_index(r, col, rows, d, x_blk)];
-  }
-  __syncthreads();
+  const int64_t rbase = (int64_t)blockIdx.x * 32 * kCoordSub;
+  const int lcol = c0 + threadIdx.x;  // the column this thread loads
   bool bad = false;
-  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-    const int col = c0 + k;
+  for (int sub = 0; sub < kCoordSub; sub++) {
+    const int64_t r0 = rbase + 32 * sub;
+    if (r0 >= rows) break;
+    float(*tb)[33] = t[sub & 1];
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+      const int64_t r = r0 + k;
+      if (r < rows && lcol < d) tb[k][threadIdx.x] = X[x_index(r, lcol, rows, d, x_blk)];
+    }
+    __syncthreads();
     const int64_t r = r0 + threadIdx.x;
-    if (r < rows && col < d) {
-      const float v = t[threadIdx.x][k];
-      bad |= !(fabsf(v) <= 3.402823466e38f);  // runtime.cpp:172 (NaN and inf)
-      const lkg::Coord co = lkg::lut_coords_fast(c.cc, ktab, kf, v);
-      uint32_t w1 = __float_as_uint(fmaf(co.w1, 32768.0f, 8388608.0f)) - 0x4B000000u;
-      int l0 = co.l0;
-      if (w1 >= 32768u) {
-        w1 = 0u;
-        l0 += 1;
+    if (r < rows) {
+      uint32_t* rp = Rt + (int64_t)(c0 + threadIdx.y) * ld + r;
+      float* sp = St + (int64_t)(c0 + threadIdx.y) * ld + r;
+      const int64_t step = (int64_t)blockDim.y * ld;
+      for (int k = threadIdx.y; k < 32 && c0 + k < d; k += blockDim.y, rp += step, sp += step) {
+        const float v = tb[threadIdx.x][k];
+        bad |= !(fabsf(v) <= 3.402823466e38f);  // runtime.cpp:172 (NaN and inf)
+        const lkg::Coord co = lkg::lut_coords_fast(c.cc, ktab, kf, v);
+        uint32_t w1 = __float_as_uint(fmaf(co.w1, 32768.0f, 8388608.0f)) - 0x4B000000u;
+        int l0 = co.l0;
+        if (w1 >= 32768u) {
+          w1 = 0u;
+          l0 += 1;
+        }
+        const uint32_t line = (uint32_t)(co.k * c.cc.L + l0);
+        *rp = w1 | (line << 15) | (co.in ? 0u : 0x80000000u);
+        // the walk's own base activation: f64 for the f64-accumulating layers, MUFU otherwise (so a
+        // layer keeps its result bits whether or not it takes the coordinate pass, e.g. column shards)
+        *sp = exact ? lkg::silu_exact(zs ? v : co.xp) : lkg::silu_fast(zs ? v : co.xp);
       }
-      const uint32_t line = (uint32_t)(co.k * c.cc.L + l0);
-      Rt[(int64_t)col * ld + r] = w1 | (line << 15) | (co.in ? 0u : 0x80000000u);
-      // the walk's own base activation: f64 for the f64-accumulating layers, MUFU otherwise (so a
-      // layer keeps its result bits whether or not it takes the coordinate pass, e.g. column shards)
-      St[(int64_t)col * ld + r] = exact ? lkg::silu_exact(zs ? v : co.xp) : lkg::silu_fast(zs ? v : co.xp);
     }
   }
   if (__any_sync(0xffffffffu, bad) && threadIdx.x == 0) atomicExch(nonfinite, 1ull);
@@ -1019,10 +1030,11 @@ void launch_forward_tiled(lkg_ctx* ctx, const lkg_layer* L, const float* X, int6
     float* St = Xt + xt_elems;
     const dim3 tgrid((unsigned)((rows + 31) / 32), (unsigned)((L->in_dim + 31) / 32));
     if (rec) {
+      const dim3 cgrid((unsigned)((rows + 32 * kCoordSub - 1) / (32 * kCoordSub)), tgrid.y);
       CoordPassArgs ca{};
       ca.cc = a.cc;
       for (int k = 0; k < a.cc.K; k++) ca.ktab[k] = a.ktab[k];
-      coord_pass_kernel<<<tgrid, dim3(32, 8), 0, ctx->stream>>>(ca, X, rows, L->in_dim, x_blk, ld,
+      coord_pass_kernel<<<cgrid, dim3(32, 8), 0, ctx->stream>>>(ca, X, rows, L->in_dim, x_blk, ld,
                                                                reinterpret_cast<uint32_t*>(Xt), St, zs, f64,
                                                                a.counters + 2);
       a.lgL = __builtin_ctz((unsigned)Ls);
