@@ -826,6 +826,34 @@ def test_chain_graph_owns_its_buffers(lk):
 
 
 @pytest.mark.gpu
+def test_chain_graph_with_input_split(lk):
+    """A captured chain whose wide layer splits its inputs (1024 -> 512 on 2048 rows: 64 items on 148
+    SMs) replays the walk, the row-flag reset and the reduce kernel; the graph owns the planes of
+    partial sums, so larger split forwards on the same engine in between do not disturb it, and the
+    OobStats of each replay are the direct call's."""
+    import torch
+    eng = lk.Engine(0)
+    chain = lk.compile_model([lk.gen_layer(31, 1024, 512, 8), lk.gen_layer(32, 512, 4, 8)], lk.QuantConfig(64),
+                             lk.OobConfig(), engine=eng)
+    X = torch.empty((2048, 1024), device="cuda").uniform_(-1.3, 1.3)
+    ref = lk.lut_model_forward_batch(chain, X, engine=eng)
+    want = ref.Y.clone()
+    Y = torch.empty((2048, 4), device="cuda")
+    g = lk.ChainGraph(chain, X, Y, engine=eng)
+    big = torch.empty((6144, 1024), device="cuda").uniform_(-1.3, 1.3)
+    for _ in range(2):
+        lk.lut_model_forward_batch(chain, big, engine=eng)      # grows the engine's own planes
+        Y.zero_()
+        g()
+        torch.cuda.synchronize()
+        assert torch.equal(Y, want)
+        st = eng.collect(2)
+        assert [(s.n_oob_samples, s.n_oob_inputs) for s in st] == \
+            [(s.n_oob_samples, s.n_oob_inputs) for s in ref.per_layer]
+    del g
+
+
+@pytest.mark.gpu
 def test_torch_inputs_are_stream_ordered(lk):
     """A torch input still being written on torch's current stream (delayed by a long-running
     kernel) is read only after that write: the engine's private stream waits on torch's stream
