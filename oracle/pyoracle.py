@@ -130,6 +130,35 @@ def build(ref: bool = True) -> None:
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 
+class _ChainSession:
+    def __init__(self, o, chain, X, tier, nthreads):
+        X = np.ascontiguousarray(X, np.float64)
+        self.o, self.rows, self.n = o, X.shape[0], len(chain)
+        arr = (_Art * len(chain))(*[a._c() for a in chain])
+        o.lib.ork_chain_session_create.restype = C.c_void_p
+        self.h = o.lib.ork_chain_session_create(arr, len(chain), _ptr(X, _f64p), self.rows, tier, nthreads)
+        if not self.h:
+            raise RuntimeError("ork_chain_session_create failed")
+        self.Y = np.zeros((self.rows, chain[-1].out_dim), np.float64)
+        self.st = np.zeros((len(chain), 4), np.uint64)
+
+    def run(self):
+        self.o._chk(self.o.lib.ork_chain_session_run(C.c_void_p(self.h), _ptr(self.Y, _f64p), _ptr(self.st, _u64p)))
+        return self.Y, self.st
+
+    def close(self):
+        if self.h:
+            self.o.lib.ork_chain_session_free.restype = None
+            self.o.lib.ork_chain_session_free(C.c_void_p(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Oracle:
     def __init__(self, kind: str = "auto"):
         if kind == "auto":
@@ -210,6 +239,14 @@ class Oracle:
         self._chk(self.lib.ork_lut_model_forward(arr, len(chain), _ptr(X, _f64p), rows, tier, nthreads,
                                                  _ptr(Y, _f64p), _ptr(st, _u64p)))
         return Y, st
+
+    def chain_session(self, chain: list[Artifact], X: np.ndarray, tier: int = 1, nthreads: int = 1):
+        """A prepared chain forward for timing (reference library only; None otherwise): artifacts
+        converted and the per-thread Matrix shards cut once, so that ``run()`` times only the threads'
+        lut_model_forward_batch calls and the copy of their results."""
+        if not hasattr(self.lib, "ork_chain_session_create"):
+            return None
+        return _ChainSession(self, chain, X, tier, nthreads)
 
     def spline_forward(self, spec: Spec, X: np.ndarray, tier: int = 1, nthreads: int = 1):
         X = np.ascontiguousarray(X, np.float64)

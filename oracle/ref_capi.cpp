@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <cstring>
 #include <exception>
+#include <memory>
+#include <stdexcept>
 #include <string>
 #include <thread>
 #include <vector>
@@ -231,6 +233,68 @@ int ork_lut_model_forward(const ork_artifact* chain, int32_t n, const double* X,
       }
   });
 }
+
+// A prepared chain forward for timing the reference fairly (bench.py's CPU legs): the artifacts are
+// converted and the batch is cut into the per-thread Matrix shards ONCE, outside the timed region —
+// what a multi-threaded caller of the reference would hold anyway; a run is then only the threads'
+// lut_model_forward_batch calls (runtime.cpp:298-314) and the copy of their results into Y.
+struct ChainSession {
+  std::vector<LutLayerArtifact> arts;
+  std::vector<Matrix> shards;
+  std::vector<std::int64_t> row0;
+  Tier tier = Tier::Optimized;
+  std::int64_t rows = 0;
+  int mo = 0;
+};
+
+void* ork_chain_session_create(const ork_artifact* chain, int32_t n, const double* X, int64_t rows, int32_t tier,
+                               int32_t nthreads) {
+  ChainSession* S = nullptr;
+  const int rc = guarded([&] {
+    auto s = std::make_unique<ChainSession>();
+    for (int l = 0; l < n; l++) s->arts.push_back(to_artifact(&chain[l]));
+    s->tier = tier ? Tier::Optimized : Tier::Scalar;
+    s->rows = rows;
+    s->mo = n > 0 ? chain[n - 1].out_dim : 0;
+    const int d = n > 0 ? chain[0].in_dim : 0;
+    int T = nthreads > 1 ? nthreads : 1;
+    if (T > rows) T = rows > 0 ? static_cast<int>(rows) : 1;
+    for (int t = 0; t < T; t++) {
+      const std::int64_t r0 = rows * t / T, r1 = rows * (t + 1) / T;
+      s->row0.push_back(r0);
+      s->shards.push_back(to_matrix(X + r0 * d, r1 - r0, d));
+    }
+    S = s.release();
+  });
+  return rc == 0 ? S : nullptr;
+}
+
+int ork_chain_session_run(void* session, double* Y, uint64_t* stats) {
+  return guarded([&] {
+    ChainSession* s = static_cast<ChainSession*>(session);
+    if (!s) throw std::invalid_argument("null chain session");
+    const int T = static_cast<int>(s->shards.size()), n = static_cast<int>(s->arts.size());
+    std::vector<std::vector<OobStats>> parts(T);
+    shard_rows(T, T, [&](std::int64_t t0, std::int64_t, int) {
+      const int t = static_cast<int>(t0);
+      ChainBatchResult r = lut_model_forward_batch(s->arts, s->shards[t], s->tier);
+      std::memcpy(Y + s->row0[t] * s->mo, r.Y.data.data(), sizeof(double) * r.Y.data.size());
+      parts[t] = r.per_layer;
+    });
+    if (stats)
+      for (int l = 0; l < n; l++) {
+        OobStats tot;
+        for (auto& p : parts)
+          if (!p.empty()) tot.merge(p[l]);
+        stats[4 * l + 0] = tot.n_samples;
+        stats[4 * l + 1] = tot.n_oob_samples;
+        stats[4 * l + 2] = tot.n_inputs;
+        stats[4 * l + 3] = tot.n_oob_inputs;
+      }
+  });
+}
+
+void ork_chain_session_free(void* session) { delete static_cast<ChainSession*>(session); }
 
 int ork_spline_forward(const ork_spec* s, const double* X, int64_t rows, int32_t tier,
                        int32_t nthreads, double* Y) {

@@ -204,3 +204,20 @@ def test_nonfinite_rejected(oracle):
     with pytest.raises(OracleError) as e:
         oracle.lut_forward(a, np.array([[-np.inf]]))
     assert e.value.code == 3
+
+
+def test_reference_chain_session_matches_direct_call():
+    """bench.py times the reference through a prepared session (artifacts converted and per-thread
+    Matrix shards cut outside the timed region): same outputs and OobStats as the direct call."""
+    from oracle.pyoracle import Oracle
+    o = Oracle("auto")
+    chain = [o.compile_layer(o.recipe_layer(2, l), 64, 1, 1, 0, 1, 0) for l in range(2)]
+    X = o.recipe_inputs(2, 0, 5001).astype(np.float64)
+    sess = o.chain_session(chain, X, 1, 3)
+    if sess is None:
+        pytest.skip("the C port has no session entry (reference library only)")
+    Y, st = o.lut_model_forward(chain, X, 1, 3)
+    for _ in range(2):
+        Y2, st2 = sess.run()
+        assert np.array_equal(Y, Y2) and np.array_equal(st, st2)
+    sess.close()
